@@ -1,0 +1,171 @@
+/*
+ * cmf_b200.h -- C ABI of the B200-native ALS half-iteration.
+ *
+ * The reference (`cmf`, /root/reference/pkg/src/cmf) has no FFI: its hot path
+ * is a set of Python functions over numba kernels.  Each entry point below is
+ * the stateless C replacement for one of those functions; the Python package
+ * paper_1808_03843_b200 keeps the reference's Python names and signatures and
+ * binds these symbols with ctypes (see INTEGRATION.md for the stub a `cmf`
+ * maintainer would add to route the reference's own functions here).
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer owned by the caller (e.g. a torch CUDA
+ *     tensor's data_ptr()), unless the parameter name ends in `_host`.
+ *   - Sizes and offsets are 64-bit.  `indptr` holds absolute positions into
+ *     `indices`/`values`, so a row block [r0, r1) is processed by passing
+ *     `indptr + r0` with `nrows = r1 - r0` (outputs offset by the caller).
+ *   - Packed symmetric storage is the reference's row-major lower triangle:
+ *     entry (i, j<=i) at i*(i+1)/2 + j (gram.py:20-21, :113-129).  `a_stride`
+ *     is the element distance between consecutive systems (>= f*(f+1)/2).
+ *   - All work is enqueued on `stream` (a cudaStream_t); nothing synchronises
+ *     except where a function documents a device->host read.
+ *   - Return value: one of the CMF_* status codes.  `cmf_last_error()` gives a
+ *     thread-local message for the last non-zero status.
+ */
+#ifndef CMF_B200_H
+#define CMF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMF_OK 0
+#define CMF_EINVAL 1     /* -> DataError            (errors.py:14-15)   */
+#define CMF_EOVERFLOW 2  /* -> NumericalError       (gram.py:139-145)   */
+#define CMF_ESINGULAR 3  /* -> SingularSystemError  (solvers.py:225-235)*/
+#define CMF_ECUDA 4      /* -> CmfError (CUDA runtime failure)          */
+
+#define CMF_PREC_FP32 0
+#define CMF_PREC_FP16 1
+
+/* Gram kernels (K1).  BITWISE reproduces the reference's float32
+ * mul-then-add in CSR order bit for bit (gram.py:149-187); FMA fuses the
+ * multiply-add (one rounding); TC runs the tcgen05 tensor-core path with
+ * fp16 operands and fp32 TMEM accumulation (CG path only). */
+#define CMF_GRAM_BITWISE 0
+#define CMF_GRAM_FMA 1
+#define CMF_GRAM_TC 2
+
+/* CG vector arithmetic.  FP32 is the paper's mixed-precision design
+ * (fp16/fp32 A, fp32 vectors); FP64 restates solvers.py:70-145 operation for
+ * operation (float64, sequential dot products) and is bitwise equal to it. */
+#define CMF_CG_FP32 0
+#define CMF_CG_FP64 1
+
+const char *cmf_last_error(void);
+int cmf_version(void);
+/* SM count and compute capability of the current device (host query). */
+int cmf_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/*
+ * K1+K2: per-row Gram matrix and right-hand side for one half-update.
+ * Replaces gram.assemble_side (gram.py:236-314) with its kernels
+ * _accumulate_chunk (gram.py:190-206), pack_half (gram.py:132-146) and
+ * _bias_chunk (gram.py:209-220) fused into one pass over the gathered rows.
+ *
+ *   A_u = base + sum_p fl(a_w[p] * theta_i) * theta_j  + reg * I
+ *   b_u = sum_p b_w[p] * theta_{indices[p]}     (float64 accumulation)
+ *   reg = float32(lam * n_u) if weighted_reg else float32(lam)
+ *
+ * a_weights NULL = all ones; b_weights NULL = skip the bias (b_out unused);
+ * base_packed NULL = zeros.  a_out is float32 or binary16 (RNE) per
+ * `precision`; a finite entry that overflows binary16 sets *overflow_flag
+ * (device int, caller zeroes it) and the call still returns CMF_OK -- the
+ * caller reads the flag and raises NumericalError.  nu_out (int64, nullable)
+ * receives n_u.  kernel: CMF_GRAM_*.
+ */
+int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices,
+                      const float *a_weights, const float *b_weights,
+                      int64_t nrows, const float *fixed, int64_t ncols, int32_t f,
+                      double lam, int32_t weighted_reg, const float *base_packed,
+                      int32_t precision, int32_t kernel, void *a_out, int64_t a_stride,
+                      float *b_out, int64_t *nu_out, int32_t *overflow_flag,
+                      void *stream);
+
+/*
+ * K2 alone: b_u = sum_p b_w[p] * theta_{indices[p]}, float64 accumulation in
+ * CSR order, rounded once to float32.  Replaces gram.get_bias /
+ * gram._bias_chunk (gram.py:209-220, :334-344).
+ */
+int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,
+                  int64_t nrows, const float *fixed, int64_t ncols, int32_t f,
+                  float *b_out, void *stream);
+
+/*
+ * K3: truncated CG on a batch of packed systems.  Replaces
+ * solvers._cg_batch (solvers.py:121-145) as called by batch_solve
+ * (solvers.py:238-245) and cg_solve/cg_solve_half (solvers.py:173-202).
+ *   eps (float64 per system, nullable): absolute residual tolerance; when NULL
+ *   the kernel uses cg_tol * ||b_s||_2 (solvers.py:240).
+ *   nu (int64, nullable): systems with nu[s] == 0 are skipped and x_out[s] is
+ *   not written (als.py:69-72 compaction, done in place).
+ *   x0 and x_out may alias (in-place warm start).  iters/broke nullable.
+ *   *breakdowns (device int, nullable) accumulates the breakdown count.
+ */
+int cmf_batch_cg(const void *a, int32_t a_precision, int64_t a_stride, const float *b,
+                 const float *x0, const double *eps, double cg_tol, const int64_t *nu,
+                 int64_t nsys, int32_t f, int32_t f_s, int32_t accum, float *x_out,
+                 int32_t *iters, int32_t *broke, int32_t *breakdowns, void *stream);
+
+/*
+ * K4: batched exact solve (Cholesky + two triangular solves) of packed
+ * float32 systems.  Replaces solvers.exact_solve (solvers.py:148-164) and the
+ * exact branch of batch_solve (solvers.py:221-237).  info[s] = 0 or k+1 for a
+ * non-positive k-th pivot (LAPACK convention); x_out[s] is not written for
+ * such systems and *nbad (device int, nullable) counts them.  nu as above.
+ * accum: CMF_CG_FP32 (float32 factorisation) or CMF_CG_FP64.
+ */
+int cmf_batch_cholesky(const float *a, int64_t a_stride, const float *b, const int64_t *nu,
+                       int64_t nsys, int32_t f, int32_t accum, float *x_out, int32_t *info,
+                       int32_t *nbad, void *stream);
+
+/*
+ * Fused half-update for the streaming row-block path: Gram (+bias) into a
+ * caller-supplied workspace, then the solve, block by block, writing the
+ * solutions into `target` in place for rows with n_u > 0.  Replaces
+ * als.update_side (als.py:54-74).  method: 0 = cg, 1 = exact.  The workspace
+ * must hold ws_rows systems of a_stride elements (fp16 or fp32 per
+ * precision) plus ws_rows*f floats (b) and ws_rows int64 (n_u).
+ */
+int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *values,
+                    int64_t nrows, const float *fixed, int64_t ncols, float *target,
+                    int32_t f, double lam, int32_t weighted_reg, int32_t method,
+                    int32_t precision, int32_t kernel, int32_t f_s, double cg_tol,
+                    int32_t accum, void *ws_a, int64_t a_stride, float *ws_b,
+                    int64_t *ws_nu, int64_t ws_rows, int32_t *flags, void *stream);
+
+/* float32 -> binary16 RNE over n elements; *overflow_flag as above.
+ * Replaces gram.pack_half (gram.py:132-146). */
+int cmf_pack_half(const float *in, void *out, int64_t n, int32_t *overflow_flag,
+                  void *stream);
+
+/*
+ * Evaluation (f2 in SURVEY 8(f)).  Squared-error partial sums of
+ * (r - x_u . theta_v) over `count` (user, item, rating) triples, float64,
+ * reduced deterministically into *out (one float64).  Replaces the data
+ * term of als.objective (als.py:77-97) and als.rmse (als.py:100-107).
+ * users/items are int64 when idx64 != 0, else int32.
+ */
+int cmf_sq_error(const void *users, const void *items, int32_t idx64, const float *ratings,
+                 int64_t count, const float *x, const float *theta, int32_t f,
+                 double *out, void *stream);
+/* Same over a CSR view (row index implied by indptr). */
+int cmf_sq_error_csr(const int64_t *indptr, const int32_t *indices, const float *values,
+                     int64_t nrows, const float *x, const float *theta, int32_t f,
+                     double *out, void *stream);
+/* sum_r weight_r * ||x_r||^2 in float64 (weight = n_r from indptr, or 1 when
+ * indptr is NULL) -> *out.  The regulariser of als.objective (als.py:86-93). */
+int cmf_weighted_sqnorm(const int64_t *indptr, const float *x, int64_t nrows, int32_t f,
+                        double *out, void *stream);
+/* pred[k] = x_{users[k]} . theta_{items[k]} (float32).  factors.predict_pairs
+ * (factors.py:41-54). */
+int cmf_predict_pairs(const void *users, const void *items, int32_t idx64, int64_t count,
+                      const float *x, const float *theta, int32_t f, float *pred,
+                      void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CMF_B200_H */

@@ -1,0 +1,338 @@
+"""Explicit-feedback ALS on the B200: the half-iteration and the epoch loop.
+
+Mirrors the reference's als.py (als.py:33-163).  ``update_side`` is the
+drop-in boundary (als.py:54-74): same signature, same in-place semantics
+(``target`` rows with n_u > 0 are overwritten, ``fixed`` is read-only), same
+return value (PhaseTimes, gram_bytes, cg_breakdowns) and errors.
+
+Per half-update the rows are processed in blocks that fit a cached HBM
+workspace (all of a Netflix side fits one block): one fused Gram+bias kernel
+writes the block's packed systems (fp16 or fp32, 16-byte aligned stride),
+then one solve kernel reads them and writes the solutions straight into
+``target`` (systems with n_u == 0 are skipped in-kernel, which is the
+reference's compaction without the copies).  ``train`` keeps the ratings,
+both factor matrices and the test set resident; only per-epoch scalars come
+back to the host.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .data import DeviceRatings, RowView, SparseRatings, Triples
+from .errors import DataError, NumericalError
+from .factors import init_factors
+from .gram import TileConfig, packed_size, roofline_estimate
+from .report import EpochRecord, PhaseTimes, TrainReport
+from .solvers import SolverConfig, _singular_error
+
+WORKSPACE_BYTES = int(float(os.environ.get("CMF_WORKSPACE_GB", "16")) * (1 << 30))
+
+
+@dataclass
+class AlsConfig:
+    f: int = 100
+    lam: float = 0.05
+    epochs: int = 10
+    solver: SolverConfig = field(default_factory=SolverConfig)
+    init_scale: float = 0.1
+    seed: int = 0
+    target_rmse: float | None = None
+    weighted_reg: bool = True
+    tiles: TileConfig = field(default_factory=TileConfig)
+    gram_kernel: str = "auto"
+
+    def __post_init__(self):
+        if self.f < 1:
+            raise DataError("f must be >= 1")
+        if self.lam < 0:
+            raise DataError("lambda must be >= 0")
+        if self.epochs < 1:
+            raise DataError("epochs must be >= 1")
+
+
+def aligned_stride(f: int) -> int:
+    """Packed row stride rounded to 8 elements (16-byte rows in fp16)."""
+    return (packed_size(f) + 7) // 8 * 8
+
+
+def resolve_gram_kernel(kernel: str | None, solver: SolverConfig) -> str:
+    if kernel in (None, "auto"):
+        return os.environ.get("CMF_TRAIN_GRAM_KERNEL", "fma")
+    if kernel not in nat.GRAM_KERNELS:
+        raise DataError(f"unknown gram kernel {kernel!r}")
+    return kernel
+
+
+class _Workspace:
+    """Per-device scratch for the packed systems of one row block."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, dev, nbytes: int) -> torch.Tensor:
+        key = (dev.index,)
+        t = self.bufs.get(key)
+        if t is None or t.numel() < nbytes:
+            self.bufs.pop(key, None)
+            t = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            self.bufs[key] = t
+        return t
+
+
+_WS = _Workspace()
+
+
+def release_workspace():
+    _WS.bufs.clear()
+
+
+def _view_dev(view: RowView, dev):
+    return (nat.to_dev(view.indptr, torch.int64, dev), nat.to_dev(view.indices, torch.int32, dev),
+            nat.to_dev(view.values, torch.float32, dev))
+
+
+class HalfUpdatePlan:
+    """Device buffers for repeated half-updates of one view: the packed-system
+    workspace (16-byte aligned stride), b, n_u and a 4-int flag block
+    (overflow, CG breakdowns, singular systems).  Launching through a plan
+    never synchronises; ``check`` reads the flags once."""
+
+    def __init__(self, nrows: int, f: int, solver: SolverConfig, dev,
+                 workspace_bytes: int | None = None):
+        self.f, self.solver, self.nrows = f, solver, nrows
+        self.half = solver.precision == "fp16"
+        self.esize = 2 if self.half else 4
+        self.stride = aligned_stride(f)
+        row_bytes = self.stride * self.esize + f * 4 + 8
+        budget = WORKSPACE_BYTES if workspace_bytes is None else int(workspace_bytes)
+        self.rows_blk = max(1, min(nrows, budget // row_bytes)) if nrows else 1
+        ws = _WS.get(dev, self.rows_blk * row_bytes)
+        rb = self.rows_blk
+        a = ws[: rb * self.stride * self.esize]
+        self.a_ws = a.view(torch.float16 if self.half else torch.float32).view(rb, self.stride)
+        off = rb * self.stride * self.esize
+        self.b_ws = ws[off: off + rb * f * 4].view(torch.float32).view(rb, f)
+        off += rb * f * 4
+        self.nu_ws = ws[off: off + rb * 8].view(torch.int64)
+        self.flags = torch.zeros(4, dtype=torch.int32, device=dev)
+
+    def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
+               row0: int = 0, nrows: int | None = None):
+        """Gram(+bias) -> solve for rows [row0, row0+nrows) of the view, block by
+        block, solutions written into tg (rows indexed like the view)."""
+        f, solver = self.f, self.solver
+        nrows = self.nrows if nrows is None else nrows
+        st = nat.stream_ptr()
+        for r0 in range(row0, row0 + nrows, self.rows_blk):
+            nb = min(self.rows_blk, row0 + nrows - r0)
+            if record is not None:
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record()
+            nat.call("cmf_gram_assemble", nat.ptr(indptr) + 8 * r0, nat.ptr(indices), None,
+                     nat.ptr(values), nb, nat.ptr(fx), fx.shape[0], f, float(lam),
+                     int(bool(weighted_reg)), None, nat.PREC[solver.precision],
+                     nat.GRAM_KERNELS[kernel], nat.ptr(self.a_ws), self.stride,
+                     nat.ptr(self.b_ws), nat.ptr(self.nu_ws), nat.ptr(self.flags), st)
+            if record is not None:
+                e1.record()
+            tgt = nat.ptr(tg) + 4 * r0 * f
+            if solver.method == "cg":
+                nat.call("cmf_batch_cg", nat.ptr(self.a_ws), nat.PREC[solver.precision],
+                         self.stride, nat.ptr(self.b_ws), tgt, None, float(solver.cg_tol),
+                         nat.ptr(self.nu_ws), nb, f, int(solver.cg_iters),
+                         nat.ACCUM[solver.accum], tgt, None, None, nat.ptr(self.flags) + 4, st)
+            else:
+                nat.call("cmf_batch_cholesky", nat.ptr(self.a_ws), self.stride,
+                         nat.ptr(self.b_ws), nat.ptr(self.nu_ws), nb, f,
+                         nat.ACCUM[solver.accum], tgt, None, nat.ptr(self.flags) + 8, st)
+            if record is not None:
+                e2.record()
+                record.setdefault("gram_" + kernel, []).append((e0, e1))
+                record.setdefault("solve_" + solver.method, []).append((e1, e2))
+
+    def read_flags(self):
+        fl = self.flags.cpu().tolist()  # synchronises
+        self.flags.zero_()
+        return fl
+
+
+def resolve_events(record: dict) -> dict:
+    """{name: [(start, end) events]} -> {name: [ms, ...]} (synchronises)."""
+    out = {}
+    for name, pairs in record.items():
+        out[name] = [a.elapsed_time(b) for a, b in pairs]
+    return out
+
+
+def update_side(view: RowView, fixed, target, lam: float, solver: SolverConfig,
+                tiles: TileConfig | None = None, weighted_reg: bool = True, *,
+                gram_kernel: str | None = None, workspace_bytes: int | None = None):
+    """One half-update; writes the solutions into ``target`` in place."""
+    if target.shape[0] != view.nrows or fixed.shape[1] != target.shape[1]:
+        raise DataError("factor matrices do not match the ratings view")
+    if view.ncols != fixed.shape[0]:
+        raise DataError(f"feature matrix has {fixed.shape[0]} rows, ratings expect {view.ncols}")
+    if tiles is not None and not isinstance(tiles, TileConfig):
+        raise DataError("tiles must be a TileConfig")
+    kernel = resolve_gram_kernel(gram_kernel, solver)
+    host = not nat.is_device(target)
+    dev = nat.device()
+    indptr, indices, values = _view_dev(view, dev)
+    fx = nat.to_dev(fixed, torch.float32, dev)
+    tg = nat.to_dev(target, torch.float32, dev) if host else target
+    if not (tg.is_contiguous() and tg.dtype == torch.float32):
+        raise DataError("device target must be a contiguous float32 tensor")
+    nrows, f = int(view.nrows), int(fx.shape[1])
+    plan = HalfUpdatePlan(nrows, f, solver, dev, workspace_bytes)
+    rec = {}
+    plan.launch(indptr, indices, values, fx, tg, lam, weighted_reg, kernel, rec)
+    fl = plan.read_flags()
+    if fl[0]:
+        raise NumericalError("Gram entries overflow binary16 range (+-65504); "
+                             "rescale the ratings before using half precision")
+    if fl[2]:
+        raise _locate_singular(indptr, indices, values, nrows, fx, f, lam, weighted_reg,
+                               kernel, solver)
+    times = PhaseTimes()
+    for name, ms in resolve_events(rec).items():
+        if name.startswith("gram"):
+            times.accumulate += sum(ms) / 1e3
+        else:
+            times.solve += sum(ms) / 1e3
+    if host:
+        if isinstance(target, torch.Tensor):
+            target.copy_(tg)
+        else:
+            target[...] = nat.to_host(tg)
+    return times, nrows * packed_size(f) * plan.esize, int(fl[1])
+
+
+def _locate_singular(indptr, indices, values, nrows, fx, f, lam, weighted_reg, kernel, solver):
+    """Recompute the side with per-system info to name the failing rows, numbered
+    among rows with n_u > 0 as the reference's compacted batch does (als.py:69-71)."""
+    dev = fx.device
+    P = packed_size(f)
+    a = torch.empty((nrows, P), dtype=torch.float32, device=dev)
+    b = torch.empty((nrows, f), dtype=torch.float32, device=dev)
+    nu = torch.empty(nrows, dtype=torch.int64, device=dev)
+    nat.call("cmf_gram_assemble", nat.ptr(indptr), nat.ptr(indices), None, nat.ptr(values), nrows,
+             nat.ptr(fx), fx.shape[0], f, float(lam), int(bool(weighted_reg)), None, 0,
+             nat.GRAM_KERNELS[kernel], nat.ptr(a), P, nat.ptr(b), nat.ptr(nu), None,
+             nat.stream_ptr())
+    out = torch.empty_like(b)
+    info = torch.zeros(nrows, dtype=torch.int32, device=dev)
+    nat.call("cmf_batch_cholesky", nat.ptr(a), P, nat.ptr(b), nat.ptr(nu), nrows, f,
+             nat.ACCUM[solver.accum], nat.ptr(out), nat.ptr(info), None, nat.stream_ptr())
+    sel = torch.nonzero(nu > 0).flatten()
+    bad = torch.nonzero(info[sel]).flatten()
+    return _singular_error(bad.cpu().tolist())
+
+
+# ------------------------------------------------------------------ evaluation
+
+def _ratings_dev(r):
+    return r if isinstance(r, DeviceRatings) else r.to_device()
+
+
+def _reduce_buf(dev):
+    return torch.empty(nat.REDUCE_SLOTS + 1, dtype=torch.float64, device=dev)
+
+
+def objective(x, theta, ratings, lam: float, weighted: bool = True) -> float:
+    """Weighted-lambda training objective in float64 (als.py:77-97), on the GPU."""
+    dev = nat.device()
+    r = _ratings_dev(ratings)
+    xd, td = nat.to_dev(x, torch.float32, dev), nat.to_dev(theta, torch.float32, dev)
+    f = int(xd.shape[1])
+    out = _reduce_buf(dev)
+    res = torch.empty(3, dtype=torch.float64, device=dev)
+    st = nat.stream_ptr()
+    nat.call("cmf_sq_error_csr", nat.ptr(r.row_ptr), nat.ptr(r.col_idx), nat.ptr(r.csr_val),
+             r.m, nat.ptr(xd), nat.ptr(td), f, nat.ptr(out), st)
+    res[0] = out[0]
+    nat.call("cmf_weighted_sqnorm", nat.ptr(r.row_ptr) if weighted else None, nat.ptr(xd), r.m, f,
+             nat.ptr(out), st)
+    res[1] = out[0]
+    nat.call("cmf_weighted_sqnorm", nat.ptr(r.col_ptr) if weighted else None, nat.ptr(td), r.n, f,
+             nat.ptr(out), st)
+    res[2] = out[0]
+    data, rx, rt = res.cpu().tolist()
+    return data + lam * (rx + rt)
+
+
+def rmse(x, theta, test: Triples) -> float:
+    """Test RMSE without clamping (als.py:100-107), on the GPU."""
+    if len(test) == 0:
+        raise DataError("cannot evaluate RMSE on an empty test set")
+    dev = nat.device()
+    xd, td = nat.to_dev(x, torch.float32, dev), nat.to_dev(theta, torch.float32, dev)
+    u = nat.to_dev(test.user, torch.int64, dev)
+    v = nat.to_dev(test.item, torch.int64, dev)
+    r = nat.to_dev(test.rating, torch.float32, dev)
+    out = _reduce_buf(dev)
+    nat.call("cmf_sq_error", nat.ptr(u), nat.ptr(v), 1, nat.ptr(r), u.shape[0], nat.ptr(xd),
+             nat.ptr(td), int(xd.shape[1]), nat.ptr(out), nat.stream_ptr())
+    return float(np.sqrt(out[0].item() / u.shape[0]))
+
+
+# ------------------------------------------------------------------- training
+
+def train(train_ratings, test, cfg: AlsConfig):
+    """ALS for cfg.epochs or until test RMSE <= cfg.target_rmse (als.py:110-157).
+
+    Host SparseRatings in -> numpy factors out; DeviceRatings in -> CUDA tensors
+    out.  Returns (X, Theta, TrainReport).
+    """
+    host = isinstance(train_ratings, SparseRatings)
+    dev = nat.device()
+    r = _ratings_dev(train_ratings)
+    m, n = r.m, r.n
+    x = nat.to_dev(init_factors(m, cfg.f, cfg.init_scale, [cfg.seed, 0]), torch.float32, dev)
+    theta = nat.to_dev(init_factors(n, cfg.f, cfg.init_scale, [cfg.seed, 1]), torch.float32, dev)
+    test_d = test.to_device() if test is not None and len(test) else None
+    nu_rows = torch.diff(r.row_ptr)
+    nu_cols = torch.diff(r.col_ptr)
+    config = asdict(cfg)
+    config["engine"] = "als"
+    report = TrainReport(engine="als", config=config,
+                         cold_rows=int((nu_rows == 0).sum().item()),
+                         cold_cols=int((nu_cols == 0).sum().item()),
+                         flops=roofline_estimate(m, n, max(r.nnz, 1), cfg.f,
+                                                 f_s=cfg.solver.cg_iters))
+    csr, csc = r.csr_view(), r.csc_view()
+    stop = "epochs"
+    for epoch in range(cfg.epochs):
+        times = PhaseTimes()
+        tx, bytes_x, brk_x = update_side(csr, theta, x, cfg.lam, cfg.solver, cfg.tiles,
+                                         cfg.weighted_reg, gram_kernel=cfg.gram_kernel)
+        times += tx
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        obj_mid = objective(x, theta, r, cfg.lam, cfg.weighted_reg)
+        e1.record()
+        tt, bytes_t, brk_t = update_side(csc, x, theta, cfg.lam, cfg.solver, cfg.tiles,
+                                         cfg.weighted_reg, gram_kernel=cfg.gram_kernel)
+        times += tt
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record()
+        obj = objective(x, theta, r, cfg.lam, cfg.weighted_reg)
+        test_rmse = rmse(x, theta, test_d) if test_d is not None else None
+        e3.record()
+        e3.synchronize()
+        times.eval += (e0.elapsed_time(e1) + e2.elapsed_time(e3)) / 1e3
+        report.gram_bytes_x, report.gram_bytes_theta = bytes_x, bytes_t
+        report.add_epoch(EpochRecord.from_phases(epoch, obj, times, objective_mid=obj_mid,
+                                                 rmse=test_rmse, cg_breakdowns=brk_x + brk_t))
+        if cfg.target_rmse is not None and test_rmse is not None and test_rmse <= cfg.target_rmse:
+            stop = "target_rmse"
+            break
+    report.stop_reason = stop
+    if host:
+        return nat.to_host(x), nat.to_host(theta), report
+    return x, theta, report

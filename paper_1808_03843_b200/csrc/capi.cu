@@ -1,0 +1,204 @@
+// extern "C" boundary (include/cmf_b200.h): argument validation, status codes,
+// thread-local error text, and dispatch to the sm_100a kernels.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace cmf {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int gram_simt_launch(const int64_t *, const int32_t *, const float *, const float *, int64_t,
+                     const float *, int, double, int, const float *, bool, bool, void *, int64_t,
+                     float *, int64_t *, int32_t *, cudaStream_t);
+int gram_tc_launch(const int64_t *, const int32_t *, const float *, const float *, int64_t,
+                   const float *, int, double, int, const float *, bool, void *, int64_t, float *,
+                   int64_t *, int32_t *, cudaStream_t);
+int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
+                     float *, cudaStream_t);
+int cg_launch(const void *, bool, int64_t, const float *, const float *, const double *, double,
+              const int64_t *, int64_t, int, int, bool, float *, int32_t *, int32_t *, int32_t *,
+              cudaStream_t);
+int chol_launch(const float *, int64_t, const float *, const int64_t *, int64_t, int, bool, float *,
+                int32_t *, int32_t *, cudaStream_t);
+int sq_error_launch(const void *, const void *, bool, const float *, int64_t, const float *,
+                    const float *, int, double *, cudaStream_t);
+int sq_error_csr_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *,
+                        const float *, int, double *, cudaStream_t);
+int wsqnorm_launch(const int64_t *, const float *, int64_t, int, double *, cudaStream_t);
+int predict_launch(const void *, const void *, bool, int64_t, const float *, const float *, int,
+                   float *, cudaStream_t);
+int pack_half_launch(const float *, void *, int64_t, int32_t *, cudaStream_t);
+
+}  // namespace cmf
+
+using namespace cmf;
+
+#define REQUIRE(cond, ...)                                  \
+    do {                                                    \
+        if (!(cond)) return set_error(CMF_EINVAL, __VA_ARGS__); \
+    } while (0)
+
+static inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char *cmf_last_error(void) { return g_err; }
+
+int cmf_version(void) { return 1; }
+
+int cmf_device_info(int *sm_count, int *cc_major, int *cc_minor) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess && sm_count) e = cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess && cc_major) e = cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e == cudaSuccess && cc_minor) e = cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (e != cudaSuccess) return set_error(CMF_ECUDA, "device query: %s", cudaGetErrorString(e));
+    return CMF_OK;
+}
+
+static int gram_dispatch(const int64_t *indptr, const int32_t *indices, const float *a_w,
+                         const float *b_w, int64_t nrows, const float *fixed, int32_t f, double lam,
+                         int32_t weighted, const float *base, int32_t precision, int32_t kernel,
+                         void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
+                         int32_t *ovf, cudaStream_t st) {
+    const bool half = precision == CMF_PREC_FP16;
+    if (kernel == CMF_GRAM_TC)
+        return gram_tc_launch(indptr, indices, a_w, b_w, nrows, fixed, f, lam, weighted, base, half,
+                              a_out, a_stride, b_out, nu_out, ovf, st);
+    return gram_simt_launch(indptr, indices, a_w, b_w, nrows, fixed, f, lam, weighted, base, half,
+                            kernel == CMF_GRAM_BITWISE, a_out, a_stride, b_out, nu_out, ovf, st);
+}
+
+int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices, const float *a_weights,
+                      const float *b_weights, int64_t nrows, const float *fixed, int64_t ncols,
+                      int32_t f, double lam, int32_t weighted_reg, const float *base_packed,
+                      int32_t precision, int32_t kernel, void *a_out, int64_t a_stride,
+                      float *b_out, int64_t *nu_out, int32_t *overflow_flag, void *stream) {
+    REQUIRE(nrows >= 0 && ncols >= 0, "negative dimensions");
+    REQUIRE(f >= 1, "f must be >= 1");
+    REQUIRE(precision == CMF_PREC_FP32 || precision == CMF_PREC_FP16, "unknown precision %d", precision);
+    REQUIRE(kernel >= CMF_GRAM_BITWISE && kernel <= CMF_GRAM_TC, "unknown gram kernel %d", kernel);
+    REQUIRE(a_stride >= f * (int64_t)(f + 1) / 2, "a_stride smaller than f*(f+1)/2");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && a_out, "null indptr / a_out");
+    REQUIRE(fixed || ncols == 0, "null fixed factors");
+    REQUIRE(!b_weights || b_out, "b_weights given without b_out");
+    return gram_dispatch(indptr, indices, a_weights, b_weights, nrows, fixed, f, lam, weighted_reg,
+                         base_packed, precision, kernel, a_out, a_stride, b_out, nu_out, overflow_flag,
+                         S(stream));
+}
+
+int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,
+                  int64_t nrows, const float *fixed, int64_t ncols, int32_t f, float *b_out,
+                  void *stream) {
+    REQUIRE(nrows >= 0 && ncols >= 0 && f >= 1, "bad dimensions");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && b_weights && b_out, "null argument");
+    return spmm_bias_launch(indptr, indices, b_weights, nrows, fixed, f, b_out, S(stream));
+}
+
+int cmf_batch_cg(const void *a, int32_t a_precision, int64_t a_stride, const float *b,
+                 const float *x0, const double *eps, double cg_tol, const int64_t *nu,
+                 int64_t nsys, int32_t f, int32_t f_s, int32_t accum, float *x_out,
+                 int32_t *iters, int32_t *broke, int32_t *breakdowns, void *stream) {
+    REQUIRE(nsys >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(f_s >= 1, "cg_iters must be >= 1");
+    REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
+    REQUIRE(a_precision == CMF_PREC_FP32 || a_precision == CMF_PREC_FP16, "unknown precision");
+    REQUIRE(accum == CMF_CG_FP32 || accum == CMF_CG_FP64, "unknown accumulation mode");
+    REQUIRE(a_stride >= f * (int64_t)(f + 1) / 2, "a_stride smaller than f*(f+1)/2");
+    if (nsys == 0) return CMF_OK;
+    REQUIRE(a && b && x0 && x_out, "null argument");
+    return cg_launch(a, a_precision == CMF_PREC_FP16, a_stride, b, x0, eps, cg_tol, nu, nsys, f, f_s,
+                     accum == CMF_CG_FP64, x_out, iters, broke, breakdowns, S(stream));
+}
+
+int cmf_batch_cholesky(const float *a, int64_t a_stride, const float *b, const int64_t *nu,
+                       int64_t nsys, int32_t f, int32_t accum, float *x_out, int32_t *info,
+                       int32_t *nbad, void *stream) {
+    REQUIRE(nsys >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(accum == CMF_CG_FP32 || accum == CMF_CG_FP64, "unknown accumulation mode");
+    REQUIRE(a_stride >= f * (int64_t)(f + 1) / 2, "a_stride smaller than f*(f+1)/2");
+    if (nsys == 0) return CMF_OK;
+    REQUIRE(a && b && x_out, "null argument");
+    return chol_launch(a, a_stride, b, nu, nsys, f, accum == CMF_CG_FP64, x_out, info, nbad, S(stream));
+}
+
+int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *values,
+                    int64_t nrows, const float *fixed, int64_t ncols, float *target, int32_t f,
+                    double lam, int32_t weighted_reg, int32_t method, int32_t precision,
+                    int32_t kernel, int32_t f_s, double cg_tol, int32_t accum, void *ws_a,
+                    int64_t a_stride, float *ws_b, int64_t *ws_nu, int64_t ws_rows, int32_t *flags,
+                    void *stream) {
+    REQUIRE(nrows >= 0 && ncols >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(method == 0 || method == 1, "unknown method %d", method);
+    REQUIRE(!(method == 1 && precision == CMF_PREC_FP16),
+            "half-precision Gram storage requires the cg solver");
+    REQUIRE(ws_rows >= 1 || nrows == 0, "empty workspace");
+    REQUIRE(flags, "null flags");
+    if (nrows == 0) return CMF_OK;
+    const size_t es = precision == CMF_PREC_FP16 ? 2 : 4;
+    cudaStream_t st = S(stream);
+    for (int64_t r0 = 0; r0 < nrows; r0 += ws_rows) {
+        const int64_t nb = nrows - r0 < ws_rows ? nrows - r0 : ws_rows;
+        int rc = cmf_gram_assemble(indptr + r0, indices, nullptr, values, nb, fixed, ncols, f, lam,
+                                   weighted_reg, nullptr, precision, kernel, ws_a, a_stride, ws_b,
+                                   ws_nu, flags + 0, stream);
+        if (rc) return rc;
+        float *tgt = target + r0 * f;
+        if (method == 0)
+            rc = cg_launch(ws_a, precision == CMF_PREC_FP16, a_stride, ws_b, tgt, nullptr, cg_tol, ws_nu,
+                           nb, f, f_s, accum == CMF_CG_FP64, tgt, nullptr, nullptr, flags + 1, st);
+        else
+            rc = chol_launch(static_cast<const float *>(ws_a), a_stride, ws_b, ws_nu, nb, f,
+                             accum == CMF_CG_FP64, tgt, nullptr, flags + 2, st);
+        if (rc) return rc;
+        (void)es;
+    }
+    return CMF_OK;
+}
+
+int cmf_pack_half(const float *in, void *out, int64_t n, int32_t *overflow_flag, void *stream) {
+    REQUIRE(n >= 0, "negative size");
+    if (n == 0) return CMF_OK;
+    REQUIRE(in && out, "null argument");
+    return pack_half_launch(in, out, n, overflow_flag, S(stream));
+}
+
+int cmf_sq_error(const void *users, const void *items, int32_t idx64, const float *ratings,
+                 int64_t count, const float *x, const float *theta, int32_t f, double *out,
+                 void *stream) {
+    REQUIRE(count >= 0 && f >= 1 && out, "bad arguments");
+    return sq_error_launch(users, items, idx64 != 0, ratings, count, x, theta, f, out, S(stream));
+}
+
+int cmf_sq_error_csr(const int64_t *indptr, const int32_t *indices, const float *values,
+                     int64_t nrows, const float *x, const float *theta, int32_t f, double *out,
+                     void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1 && out, "bad arguments");
+    return sq_error_csr_launch(indptr, indices, values, nrows, x, theta, f, out, S(stream));
+}
+
+int cmf_weighted_sqnorm(const int64_t *indptr, const float *x, int64_t nrows, int32_t f,
+                        double *out, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1 && out, "bad arguments");
+    return wsqnorm_launch(indptr, x, nrows, f, out, S(stream));
+}
+
+int cmf_predict_pairs(const void *users, const void *items, int32_t idx64, int64_t count,
+                      const float *x, const float *theta, int32_t f, float *pred, void *stream) {
+    REQUIRE(count >= 0 && f >= 1, "bad arguments");
+    return predict_launch(users, items, idx64 != 0, count, x, theta, f, pred, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,300 @@
+"""Rating data: triples, the paired CSR/CSC structure, and the synthetic
+generators the benchmark protocol uses.
+
+Mirrors the reference's data.py (Triples, RowView, SparseRatings, build,
+split_holdout, gen_synthetic; data.py:52-130, :205-302).  ``build`` runs on the
+GPU (stable device sorts + bincount scans) and is bit-identical to the
+reference's lexsort/bincount construction: the CSR order is (user, item,
+position) with the LAST duplicate kept, the CSC order is (item, user).
+``gen_synthetic``/``split_holdout`` keep the reference's numpy PCG64 draw
+sequence (identical inputs are part of the parity contract), while
+``gen_synthetic_device`` is the fast on-GPU generator used for benchmark
+shapes that the reference generator cannot reach (Netflix and up).
+
+A ``DeviceRatings`` holds the same six arrays as CUDA tensors; it is what the
+training loop keeps resident in HBM.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, NamedTuple
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import DataError
+from .factors import predict_pairs
+
+
+class RatingTriple(NamedTuple):
+    user: int
+    item: int
+    rating: float
+
+
+@dataclass
+class Triples:
+    """Flat (user, item, rating) arrays in file order (int64, int64, float32)."""
+
+    user: object
+    item: object
+    rating: object
+
+    @classmethod
+    def from_iter(cls, triples: Iterable) -> "Triples":
+        rows = list(triples)
+        u = np.array([t[0] for t in rows], dtype=np.int64)
+        v = np.array([t[1] for t in rows], dtype=np.int64)
+        r = np.array([t[2] for t in rows], dtype=np.float32)
+        return cls(u, v, r)
+
+    def __len__(self):
+        return int(self.user.shape[0])
+
+    def __getitem__(self, i):
+        return RatingTriple(int(self.user[i]), int(self.item[i]), float(self.rating[i]))
+
+    def __iter__(self):
+        for k in range(len(self)):
+            yield self[k]
+
+    def to_device(self) -> "Triples":
+        return Triples(nat.to_dev(self.user, torch.int64), nat.to_dev(self.item, torch.int64),
+                       nat.to_dev(self.rating, torch.float32))
+
+
+class RowView(NamedTuple):
+    """One orientation of the rating matrix (data.py:79-86)."""
+
+    indptr: object
+    indices: object
+    values: object
+    nrows: int
+    ncols: int
+
+
+@dataclass(frozen=True)
+class SparseRatings:
+    """Host copy of the paired CSR + CSC structure (data.py:89-130)."""
+
+    m: int
+    n: int
+    nnz: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    csr_val: np.ndarray
+    col_ptr: np.ndarray
+    row_idx: np.ndarray
+    csc_val: np.ndarray
+
+    def csr_view(self) -> RowView:
+        return RowView(self.row_ptr, self.col_idx, self.csr_val, self.m, self.n)
+
+    def csc_view(self) -> RowView:
+        return RowView(self.col_ptr, self.row_idx, self.csc_val, self.n, self.m)
+
+    def row(self, u: int):
+        lo, hi = int(self.row_ptr[u]), int(self.row_ptr[u + 1])
+        return self.col_idx[lo:hi], self.csr_val[lo:hi]
+
+    def col(self, v: int):
+        lo, hi = int(self.col_ptr[v]), int(self.col_ptr[v + 1])
+        return self.row_idx[lo:hi], self.csc_val[lo:hi]
+
+    def to_triples(self) -> Triples:
+        users = np.repeat(np.arange(self.m, dtype=np.int64), np.diff(self.row_ptr))
+        return Triples(users, self.col_idx.astype(np.int64), self.csr_val.copy())
+
+    @property
+    def nbytes(self) -> int:
+        return int(sum(getattr(self, k).nbytes for k in _ARRAYS))
+
+    def to_device(self) -> "DeviceRatings":
+        dt = {"row_ptr": torch.int64, "col_ptr": torch.int64, "col_idx": torch.int32,
+              "row_idx": torch.int32, "csr_val": torch.float32, "csc_val": torch.float32}
+        return DeviceRatings(self.m, self.n, self.nnz,
+                             **{k: nat.to_dev(getattr(self, k), dt[k]) for k in _ARRAYS})
+
+
+_ARRAYS = ("row_ptr", "col_idx", "csr_val", "col_ptr", "row_idx", "csc_val")
+
+
+@dataclass(frozen=True)
+class DeviceRatings:
+    """The same six arrays resident in HBM (torch CUDA tensors)."""
+
+    m: int
+    n: int
+    nnz: int
+    row_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    csr_val: torch.Tensor
+    col_ptr: torch.Tensor
+    row_idx: torch.Tensor
+    csc_val: torch.Tensor
+
+    def csr_view(self) -> RowView:
+        return RowView(self.row_ptr, self.col_idx, self.csr_val, self.m, self.n)
+
+    def csc_view(self) -> RowView:
+        return RowView(self.col_ptr, self.row_idx, self.csc_val, self.n, self.m)
+
+    @property
+    def nbytes(self) -> int:
+        return int(sum(t.numel() * t.element_size() for t in (getattr(self, k) for k in _ARRAYS)))
+
+    def to_host(self) -> SparseRatings:
+        return SparseRatings(self.m, self.n, self.nnz,
+                             **{k: nat.to_host(getattr(self, k)) for k in _ARRAYS})
+
+    def to_device(self) -> "DeviceRatings":
+        return self
+
+
+@dataclass
+class SyntheticTruth:
+    x_true: np.ndarray
+    theta_true: np.ndarray
+    noise_sigma: float
+
+
+# ------------------------------------------------------------------- build
+
+def _as_triples(triples) -> Triples:
+    return triples if isinstance(triples, Triples) else Triples.from_iter(triples)
+
+
+def build_device(triples, m: int | None = None, n: int | None = None) -> DeviceRatings:
+    """CSR + CSC on the GPU; bit-identical to reference data.build (data.py:205-249)."""
+    t = _as_triples(triples)
+    dev = nat.device()
+    user = nat.to_dev(t.user, torch.int64, dev)
+    item = nat.to_dev(t.item, torch.int64, dev)
+    val = nat.to_dev(t.rating, torch.float32, dev)
+    k = user.shape[0]
+    if m is None:
+        m = int(user.max().item()) + 1 if k else 0
+    if n is None:
+        n = int(item.max().item()) + 1 if k else 0
+    if k:
+        bad = (user < 0) | (user >= m) | (item < 0) | (item >= n)
+        if bool(bad.any()):
+            i = int(torch.argmax(bad.to(torch.int8)).item())
+            raise DataError(f"triple ({int(user[i])}, {int(item[i])}, {float(val[i])}) "
+                            f"out of range for a {m}x{n} matrix")
+        # stable sort on the (user, item) key keeps file order inside duplicate runs
+        key = user * n + item
+        skey, order = torch.sort(key, stable=True)
+        last = torch.ones(k, dtype=torch.bool, device=dev)
+        last[:-1] = skey[:-1] != skey[1:]
+        order = order[last]
+        su, si, sv = user[order], item[order], val[order]
+    else:
+        su = si = torch.empty(0, dtype=torch.int64, device=dev)
+        sv = torch.empty(0, dtype=torch.float32, device=dev)
+    nnz = int(su.shape[0])
+    row_ptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+    col_ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    if nnz:
+        torch.cumsum(torch.bincount(su, minlength=m), 0, out=row_ptr[1:])
+        torch.cumsum(torch.bincount(si, minlength=n), 0, out=col_ptr[1:])
+        _, corder = torch.sort(si, stable=True)
+    else:
+        corder = torch.empty(0, dtype=torch.int64, device=dev)
+    return DeviceRatings(m, n, nnz, row_ptr, si.to(torch.int32), sv, col_ptr,
+                         su[corder].to(torch.int32), sv[corder])
+
+
+def build(triples, m: int | None = None, n: int | None = None) -> SparseRatings:
+    """Reference-compatible ``build``: device construction, host arrays back."""
+    return build_device(triples, m, n).to_host()
+
+
+# --------------------------------------------------------- split / synthesis
+
+def split_holdout(triples: Triples, test_fraction: float, seed: int):
+    """Deterministic disjoint split (data.py:252-267): the reference's PCG64
+    permutation, first round(frac*N) positions -> test, both sorted."""
+    if not (0.0 < test_fraction < 1.0):
+        raise DataError(f"test_fraction must be in (0, 1), got {test_fraction}")
+    total = len(triples)
+    k = int(round(test_fraction * total))
+    perm = np.random.default_rng(seed).permutation(total)
+    parts = (np.sort(perm[k:]), np.sort(perm[:k]))
+    u, v, r = (np.asarray(a) for a in (triples.user, triples.item, triples.rating))
+    return tuple(Triples(u[ix], v[ix], r[ix]) for ix in parts)
+
+
+def gen_synthetic(m, n, f, density, noise_sigma, seed):
+    """Low-rank-plus-noise ratings with the reference's draw sequence
+    (data.py:270-302): x_true, theta_true ~ U[-0.5, 0.5) float32, k distinct
+    positions by ``choice(m*n, k, replace=False)``, rating = float32 dot
+    (+ N(0, sigma) via float64)."""
+    if not (0.0 < density <= 1.0):
+        raise DataError(f"density must be in (0, 1], got {density}")
+    if f < 1:
+        raise DataError("f must be >= 1")
+    k = int(round(density * m * n))
+    if k < 1:
+        raise DataError(f"density {density} yields no entries for a {m}x{n} matrix")
+    rng = np.random.default_rng(seed)
+    x_true = (rng.random((m, f), dtype=np.float32) - np.float32(0.5)).astype(np.float32)
+    t_true = (rng.random((n, f), dtype=np.float32) - np.float32(0.5)).astype(np.float32)
+    cells = np.sort(rng.choice(m * n, size=k, replace=False))
+    users, items = (cells // n).astype(np.int64), (cells % n).astype(np.int64)
+    ratings = _host_dot(x_true, t_true, users, items)
+    if noise_sigma > 0:
+        ratings = (ratings.astype(np.float64) + rng.normal(0.0, noise_sigma, size=k)).astype(np.float32)
+    return Triples(users, items, ratings), SyntheticTruth(x_true, t_true, noise_sigma)
+
+
+def _host_dot(x, t, users, items, chunk=1 << 18):
+    # the reference's predict_pairs arithmetic (float32 einsum per chunk); kept on
+    # the host so generated inputs are bit-identical to the reference's
+    out = np.empty(users.shape[0], dtype=np.float32)
+    for lo in range(0, users.shape[0], chunk):
+        hi = min(lo + chunk, users.shape[0])
+        out[lo:hi] = np.einsum("ij,ij->i", x[users[lo:hi]], t[items[lo:hi]])
+    return out
+
+
+def gen_synthetic_device(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1,
+                         test_fraction: float = 0.1, seed: int = 0, row_chunk: int | None = None):
+    """Fast on-GPU generator for benchmark shapes (Netflix / Yahoo / Hugewiki).
+
+    Same model as ``gen_synthetic`` -- U[-0.5, 0.5) truth factors, uniformly
+    random distinct cells, float32 dot + N(0, sigma) -- but cells are drawn
+    per row block as independent Bernoulli(p) with p = nnz_total/(m*n), where
+    nnz_total = nnz/(1-test_fraction), and a Bernoulli(test_fraction) mask
+    makes the holdout.  Train nnz is therefore nnz +- O(sqrt(nnz)).  Not
+    bit-identical to the reference generator (which cannot reach these sizes
+    on a 62 GB host); returns (DeviceRatings train, Triples test on device).
+    """
+    dev = nat.device()
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    total = nnz / (1.0 - test_fraction)
+    p = total / (float(m) * float(n))
+    xt = torch.rand((m, f), generator=g, device=dev) - 0.5
+    tt = torch.rand((n, f), generator=g, device=dev) - 0.5
+    if row_chunk is None:
+        row_chunk = max(1, (1 << 28) // max(n, 1))
+    us, vs = [], []
+    for r0 in range(0, m, row_chunk):
+        r1 = min(m, r0 + row_chunk)
+        mask = torch.rand((r1 - r0, n), generator=g, device=dev) < p
+        nzr, nzc = torch.nonzero(mask, as_tuple=True)
+        us.append(nzr.to(torch.int64) + r0)
+        vs.append(nzc.to(torch.int64))
+        del mask
+    users, items = torch.cat(us), torch.cat(vs)
+    del us, vs
+    ratings = predict_pairs(xt, tt, users, items)
+    ratings = ratings + noise_sigma * torch.randn(ratings.shape, generator=g, device=dev)
+    is_test = torch.rand(users.shape, generator=g, device=dev) < test_fraction
+    test = Triples(users[is_test], items[is_test], ratings[is_test])
+    keep = ~is_test
+    train = build_device(Triples(users[keep], items[keep], ratings[keep]), m, n)
+    return train, test

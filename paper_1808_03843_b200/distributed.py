@@ -1,0 +1,139 @@
+"""Multi-GPU ALS driver: users (CSR rows) and items (CSC rows)
+are split into contiguous nnz-balanced ranges, one range per rank (one
+process per GPU, torch.distributed over NCCL / NVLink).  Each rank keeps only
+its byte-exact slices of the CSR and CSC arrays (pointers rebased), plus full
+replicas of X and Theta.  An iteration is
+
+    update-X on my user rows  ->  all-gather X  ->  update-Theta on my item rows
+    ->  all-gather Theta
+
+which is the reference's epoch barrier (als.py:132-140) with the exchange
+inserted where the other half first reads the updated matrix.  With one rank
+there is no collective at all.
+
+Shard boundaries: r_s = searchsorted(indptr, s * nnz / k, "left") -- a pure
+function of the pointer array, so every rank computes the same plan without
+communication, and concatenating the shards reproduces the reference arrays
+exactly (tests/test_distributed.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .als import HalfUpdatePlan, resolve_gram_kernel
+from .errors import DataError, NumericalError
+
+
+def shard_bounds(indptr, world: int) -> list[int]:
+    """Row boundaries [b_0=0, ..., b_k=nrows] balancing stored ratings."""
+    ptr = indptr.cpu().numpy() if isinstance(indptr, torch.Tensor) else np.asarray(indptr)
+    nrows = ptr.shape[0] - 1
+    nnz = int(ptr[-1])
+    bounds = [0]
+    for s in range(1, world):
+        b = int(np.searchsorted(ptr, s * nnz / world, side="left"))
+        bounds.append(min(max(b, bounds[-1]), nrows))
+    bounds.append(nrows)
+    return bounds
+
+
+def shard_view(indptr, indices, values, lo: int, hi: int):
+    """Rows [lo, hi) as a self-contained view with rebased pointers."""
+    p0 = int(indptr[lo])
+    p1 = int(indptr[hi])
+    ptr = indptr[lo:hi + 1] - p0
+    return ptr, indices[p0:p1], values[p0:p1]
+
+
+class RowGather:
+    """All-gather of row blocks of a (rows, f) matrix whose rank-s block is
+    rows [b_s, b_{s+1}).  Uneven blocks are padded to the largest one for a
+    single all_gather_into_tensor, then unpacked in place."""
+
+    def __init__(self, bounds, f, device, dtype=torch.float32):
+        self.bounds = bounds
+        self.world = len(bounds) - 1
+        self.maxrows = max(bounds[i + 1] - bounds[i] for i in range(self.world))
+        self.buf = torch.empty((self.world, self.maxrows, f), dtype=dtype, device=device)
+        self.equal = all(bounds[i + 1] - bounds[i] == self.maxrows for i in range(self.world))
+
+    def __call__(self, full: torch.Tensor, rank: int, group=None):
+        import torch.distributed as dist
+        lo, hi = self.bounds[rank], self.bounds[rank + 1]
+        if self.equal and full.is_contiguous():
+            dist.all_gather_into_tensor(full[: self.world * self.maxrows].view(-1),
+                                        full[lo:hi].reshape(-1), group=group)
+            return
+        self.buf[rank, : hi - lo].copy_(full[lo:hi])
+        dist.all_gather_into_tensor(self.buf.view(-1), self.buf[rank].reshape(-1).clone(),
+                                    group=group)
+        for s in range(self.world):
+            a, b = self.bounds[s], self.bounds[s + 1]
+            if s != rank and b > a:
+                full[a:b].copy_(self.buf[s, : b - a])
+
+
+class ShardedALS:
+    """Row-sharded ALS iteration over `world` ranks (world == 1: plain device ALS)."""
+
+    def __init__(self, ratings, f: int, lam: float, solver, gram_kernel: str = "auto",
+                 rank: int = 0, world: int = 1, weighted_reg: bool = True, group=None):
+        self.f, self.lam, self.solver = f, lam, solver
+        self.weighted_reg = weighted_reg
+        self.rank, self.world, self.group = rank, world, group
+        self.gram_kernel = resolve_gram_kernel(gram_kernel, solver)
+        dev = ratings.row_ptr.device
+        self.m, self.n = ratings.m, ratings.n
+        self.xb = shard_bounds(ratings.row_ptr, world)
+        self.tb = shard_bounds(ratings.col_ptr, world)
+        xs = (self.xb[rank], self.xb[rank + 1])
+        ts = (self.tb[rank], self.tb[rank + 1])
+        self.x_view = shard_view(ratings.row_ptr, ratings.col_idx, ratings.csr_val, *xs)
+        self.t_view = shard_view(ratings.col_ptr, ratings.row_idx, ratings.csc_val, *ts)
+        self.x_plan = HalfUpdatePlan(xs[1] - xs[0], f, solver, dev)
+        self.t_plan = HalfUpdatePlan(ts[1] - ts[0], f, solver, dev)
+        if world > 1:
+            self.x_gather = RowGather(self.xb, f, dev)
+            self.t_gather = RowGather(self.tb, f, dev)
+
+    def local_nnz(self):
+        return {"x": int(self.x_view[0][-1]), "t": int(self.t_view[0][-1])}
+
+    def local_rows(self):
+        return {"x": self.xb[self.rank + 1] - self.xb[self.rank],
+                "t": self.tb[self.rank + 1] - self.tb[self.rank]}
+
+    def _half(self, plan, view, fixed, target, lo, record):
+        ptr, idx, val = view
+        # the plan writes rows [0, nrows) of the view; point it at target[lo:]
+        plan.launch(ptr, idx, val, fixed, target[lo:], self.lam, self.weighted_reg,
+                    self.gram_kernel, record)
+
+    def iteration(self, x: torch.Tensor, theta: torch.Tensor, record: dict | None = None):
+        self._half(self.x_plan, self.x_view, theta, x, self.xb[self.rank], record)
+        if self.world > 1:
+            self._gather(self.x_gather, x, record)
+        self._half(self.t_plan, self.t_view, x, theta, self.tb[self.rank], record)
+        if self.world > 1:
+            self._gather(self.t_gather, theta, record)
+
+    def _gather(self, g, full, record):
+        if record is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        g(full, self.rank, self.group)
+        if record is not None:
+            e1.record()
+            record.setdefault("allgather", []).append((e0, e1))
+
+    def check(self):
+        """Read the accumulated device flags once (synchronises)."""
+        fx, ft = self.x_plan.read_flags(), self.t_plan.read_flags()
+        if fx[0] or ft[0]:
+            raise NumericalError("Gram entries overflow binary16 range (+-65504); "
+                                 "rescale the ratings before using half precision")
+        if fx[2] or ft[2]:
+            raise DataError("singular system(s) during sharded training")
+        return fx[1] + ft[1]
