@@ -42,8 +42,10 @@ extern "C" {
 
 /* Gram kernels (K1).  BITWISE reproduces the reference's float32
  * mul-then-add in CSR order bit for bit (gram.py:149-187); FMA fuses the
- * multiply-add (one rounding); TC runs the tcgen05 tensor-core path with
- * fp16 operands and fp32 TMEM accumulation (CG path only). */
+ * multiply-add (one rounding).  The tcgen05 tensor-core path (fp16 operands,
+ * fp32 TMEM accumulation; CG route) has its own entry point,
+ * cmf_gram_assemble_tc, because it reads a binary16 shadow of the fixed
+ * factors; CMF_GRAM_TC is accepted only by cmf_half_update. */
 #define CMF_GRAM_BITWISE 0
 #define CMF_GRAM_FMA 1
 #define CMF_GRAM_TC 2
@@ -83,6 +85,25 @@ int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices,
                       int32_t precision, int32_t kernel, void *a_out, int64_t a_stride,
                       float *b_out, int64_t *nu_out, int32_t *overflow_flag,
                       void *stream);
+
+/*
+ * K1+K2 on the tensor cores (tcgen05.mma kind::f16, TMEM accumulators).
+ * Same contract as cmf_gram_assemble with a_weights == NULL, except that the
+ * fixed factors are read from `fixed16`, the binary16 shadow written by
+ * cmf_factors_to_half (row width `w16` = cmf_tc_width(f) halves), and the bias
+ * accumulates in fp32 in the same MMAs.  Requires f <= 126, 16-byte aligned
+ * a_out rows (a_stride * sizeof(elem) % 16 == 0).
+ */
+int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const float *b_weights,
+                         int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
+                         int32_t weighted_reg, const float *base_packed, int32_t precision,
+                         void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
+                         int32_t *overflow_flag, void *stream);
+/* Row width (halves) of the binary16 factor shadow for a given f. */
+int cmf_tc_width(int32_t f);
+/* fp32 (rows, f) -> binary16 (rows, w16), RNE, zero padded columns. */
+int cmf_factors_to_half(const float *x, int64_t rows, int32_t f, void *out16, int32_t w16,
+                        void *stream);
 
 /*
  * K2 alone: b_u = sum_p b_w[p] * theta_{indices[p]}, float64 accumulation in
@@ -127,14 +148,17 @@ int cmf_batch_cholesky(const float *a, int64_t a_stride, const float *b, const i
  * solutions into `target` in place for rows with n_u > 0.  Replaces
  * als.update_side (als.py:54-74).  method: 0 = cg, 1 = exact.  The workspace
  * must hold ws_rows systems of a_stride elements (fp16 or fp32 per
- * precision) plus ws_rows*f floats (b) and ws_rows int64 (n_u).
+ * precision) plus ws_rows*f floats (b) and ws_rows int64 (n_u).  With
+ * kernel == CMF_GRAM_TC, ws16 must hold ncols * cmf_tc_width(f) halves for
+ * the binary16 shadow of `fixed` (ignored otherwise).
+ * flags (4 device ints): [0] fp16 overflow, [1] CG breakdowns, [2] singular.
  */
 int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *values,
                     int64_t nrows, const float *fixed, int64_t ncols, float *target,
                     int32_t f, double lam, int32_t weighted_reg, int32_t method,
                     int32_t precision, int32_t kernel, int32_t f_s, double cg_tol,
                     int32_t accum, void *ws_a, int64_t a_stride, float *ws_b,
-                    int64_t *ws_nu, int64_t ws_rows, int32_t *flags, void *stream);
+                    int64_t *ws_nu, int64_t ws_rows, void *ws16, int32_t *flags, void *stream);
 
 /* float32 -> binary16 RNE over n elements; *overflow_flag as above.
  * Replaces gram.pack_half (gram.py:132-146). */

@@ -34,6 +34,10 @@ _SIGNATURES = {
     "cmf_device_info": (ctypes.c_int, [_vp, _vp, _vp]),
     "cmf_gram_assemble": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i32, _f64, _i32,
                                          _vp, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "cmf_gram_assemble_tc": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i32, _i32, _f64, _i32, _vp,
+                                            _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "cmf_tc_width": (ctypes.c_int, [_i32]),
+    "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
     "cmf_spmm_bias": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),
     "cmf_batch_cg": (ctypes.c_int, [_vp, _i32, _i64, _vp, _vp, _vp, _f64, _vp, _i64, _i32, _i32,
                                     _i32, _vp, _vp, _vp, _vp, _vp]),
@@ -41,7 +45,7 @@ _SIGNATURES = {
                                           _vp]),
     "cmf_half_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i32, _f64, _i32,
                                        _i32, _i32, _i32, _i32, _f64, _i32, _vp, _i64, _vp, _vp,
-                                       _i64, _vp, _vp]),
+                                       _i64, _vp, _vp, _vp]),
     "cmf_pack_half": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "cmf_sq_error": (ctypes.c_int, [_vp, _vp, _i32, _vp, _i64, _vp, _vp, _i32, _vp, _vp]),
     "cmf_sq_error_csr": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp]),
@@ -96,7 +100,7 @@ def check(rc: int, what: str = ""):
 
 # Kernel-launching entry points called since the counter was last reset (the
 # benchmark's "gpu_launches" claim counts launches of OUR kernels).
-_LAUNCH_COST = {"cmf_gram_assemble": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
+_LAUNCH_COST = {"cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
                 "cmf_batch_cholesky": 1, "cmf_pack_half": 1, "cmf_sq_error": 2,
                 "cmf_sq_error_csr": 2, "cmf_weighted_sqnorm": 2, "cmf_predict_pairs": 1}
 LAUNCHES = [0]
@@ -109,6 +113,11 @@ def call(name: str, *args):
 
 
 # ---------------------------------------------------------------- tensors
+
+def tc_width(f: int) -> int:
+    """Row width (halves) of the binary16 factor shadow the tensor-core Gram reads."""
+    return ((f + 2 + 7) // 8) * 8
+
 
 def device() -> torch.device:
     lib()

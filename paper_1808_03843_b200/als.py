@@ -121,6 +121,16 @@ class HalfUpdatePlan:
         off += rb * f * 4
         self.nu_ws = ws[off: off + rb * 8].view(torch.int64)
         self.flags = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.w16 = nat.tc_width(f)
+        self.shadow = None  # binary16 copy of the fixed factors (tensor-core Gram)
+
+    def _shadow(self, fx):
+        need = fx.shape[0] * self.w16
+        if self.shadow is None or self.shadow.numel() < need:
+            self.shadow = torch.empty(need, dtype=torch.float16, device=fx.device)
+        nat.call("cmf_factors_to_half", nat.ptr(fx), fx.shape[0], self.f, nat.ptr(self.shadow),
+                 self.w16, nat.stream_ptr())
+        return self.shadow
 
     def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
                row0: int = 0, nrows: int | None = None):
@@ -129,16 +139,31 @@ class HalfUpdatePlan:
         f, solver = self.f, self.solver
         nrows = self.nrows if nrows is None else nrows
         st = nat.stream_ptr()
+        if record is not None and kernel == "tc":
+            es0 = torch.cuda.Event(enable_timing=True)
+            es0.record()
+        shadow = self._shadow(fx) if kernel == "tc" else None
+        if record is not None and kernel == "tc":
+            es1 = torch.cuda.Event(enable_timing=True)
+            es1.record()
+            record.setdefault("shadow16", []).append((es0, es1))
         for r0 in range(row0, row0 + nrows, self.rows_blk):
             nb = min(self.rows_blk, row0 + nrows - r0)
             if record is not None:
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record()
-            nat.call("cmf_gram_assemble", nat.ptr(indptr) + 8 * r0, nat.ptr(indices), None,
-                     nat.ptr(values), nb, nat.ptr(fx), fx.shape[0], f, float(lam),
-                     int(bool(weighted_reg)), None, nat.PREC[solver.precision],
-                     nat.GRAM_KERNELS[kernel], nat.ptr(self.a_ws), self.stride,
-                     nat.ptr(self.b_ws), nat.ptr(self.nu_ws), nat.ptr(self.flags), st)
+            if kernel == "tc":
+                nat.call("cmf_gram_assemble_tc", nat.ptr(indptr) + 8 * r0, nat.ptr(indices),
+                         nat.ptr(values), nb, nat.ptr(shadow), self.w16, f, float(lam),
+                         int(bool(weighted_reg)), None, nat.PREC[solver.precision],
+                         nat.ptr(self.a_ws), self.stride, nat.ptr(self.b_ws),
+                         nat.ptr(self.nu_ws), nat.ptr(self.flags), st)
+            else:
+                nat.call("cmf_gram_assemble", nat.ptr(indptr) + 8 * r0, nat.ptr(indices), None,
+                         nat.ptr(values), nb, nat.ptr(fx), fx.shape[0], f, float(lam),
+                         int(bool(weighted_reg)), None, nat.PREC[solver.precision],
+                         nat.GRAM_KERNELS[kernel], nat.ptr(self.a_ws), self.stride,
+                         nat.ptr(self.b_ws), nat.ptr(self.nu_ws), nat.ptr(self.flags), st)
             if record is not None:
                 e1.record()
             tgt = nat.ptr(tg) + 4 * r0 * f

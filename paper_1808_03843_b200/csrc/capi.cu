@@ -20,9 +20,11 @@ int set_error(int code, const char *fmt, ...) {
 int gram_simt_launch(const int64_t *, const int32_t *, const float *, const float *, int64_t,
                      const float *, int, double, int, const float *, bool, bool, void *, int64_t,
                      float *, int64_t *, int32_t *, cudaStream_t);
-int gram_tc_launch(const int64_t *, const int32_t *, const float *, const float *, int64_t,
-                   const float *, int, double, int, const float *, bool, void *, int64_t, float *,
-                   int64_t *, int32_t *, cudaStream_t);
+int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int, int,
+                   double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
+                   cudaStream_t);
+int gram_tc_width(int f);
+int factors_to_half_launch(const float *, int64_t, int, void *, int, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
                      float *, cudaStream_t);
 int cg_launch(const void *, bool, int64_t, const float *, const float *, const double *, double,
@@ -73,8 +75,7 @@ static int gram_dispatch(const int64_t *indptr, const int32_t *indices, const fl
                          int32_t *ovf, cudaStream_t st) {
     const bool half = precision == CMF_PREC_FP16;
     if (kernel == CMF_GRAM_TC)
-        return gram_tc_launch(indptr, indices, a_w, b_w, nrows, fixed, f, lam, weighted, base, half,
-                              a_out, a_stride, b_out, nu_out, ovf, st);
+        return set_error(CMF_EINVAL, "use cmf_gram_assemble_tc for the tensor-core kernel");
     return gram_simt_launch(indptr, indices, a_w, b_w, nrows, fixed, f, lam, weighted, base, half,
                             kernel == CMF_GRAM_BITWISE, a_out, a_stride, b_out, nu_out, ovf, st);
 }
@@ -98,12 +99,37 @@ int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices, const float
                          S(stream));
 }
 
+int cmf_tc_width(int32_t f) { return gram_tc_width(f); }
+
+int cmf_factors_to_half(const float *x, int64_t rows, int32_t f, void *out16, int32_t w16,
+                        void *stream) {
+    REQUIRE(rows >= 0 && f >= 1 && w16 >= f, "bad dimensions");
+    if (rows == 0) return CMF_OK;
+    REQUIRE(x && out16, "null argument");
+    return factors_to_half_launch(x, rows, f, out16, w16, S(stream));
+}
+
+int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const float *b_weights,
+                         int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
+                         int32_t weighted_reg, const float *base_packed, int32_t precision,
+                         void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
+                         int32_t *overflow_flag, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(precision == CMF_PREC_FP32 || precision == CMF_PREC_FP16, "unknown precision %d", precision);
+    REQUIRE(a_stride >= f * (int64_t)(f + 1) / 2, "a_stride smaller than f*(f+1)/2");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && a_out && fixed16, "null argument");
+    return gram_tc_launch(indptr, indices, b_weights, nrows, fixed16, w16, f, lam, weighted_reg,
+                          base_packed, precision == CMF_PREC_FP16, a_out, a_stride, b_out, nu_out,
+                          overflow_flag, S(stream));
+}
+
 int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,
                   int64_t nrows, const float *fixed, int64_t ncols, int32_t f, float *b_out,
                   void *stream) {
     REQUIRE(nrows >= 0 && ncols >= 0 && f >= 1, "bad dimensions");
     if (nrows == 0) return CMF_OK;
-    REQUIRE(indptr && b_weights && b_out, "null argument");
+    REQUIRE(indptr && b_out, "null argument");
     return spmm_bias_launch(indptr, indices, b_weights, nrows, fixed, f, b_out, S(stream));
 }
 
@@ -138,8 +164,8 @@ int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *
                     int64_t nrows, const float *fixed, int64_t ncols, float *target, int32_t f,
                     double lam, int32_t weighted_reg, int32_t method, int32_t precision,
                     int32_t kernel, int32_t f_s, double cg_tol, int32_t accum, void *ws_a,
-                    int64_t a_stride, float *ws_b, int64_t *ws_nu, int64_t ws_rows, int32_t *flags,
-                    void *stream) {
+                    int64_t a_stride, float *ws_b, int64_t *ws_nu, int64_t ws_rows, void *ws16,
+                    int32_t *flags, void *stream) {
     REQUIRE(nrows >= 0 && ncols >= 0 && f >= 1, "bad dimensions");
     REQUIRE(method == 0 || method == 1, "unknown method %d", method);
     REQUIRE(!(method == 1 && precision == CMF_PREC_FP16),
@@ -147,13 +173,22 @@ int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *
     REQUIRE(ws_rows >= 1 || nrows == 0, "empty workspace");
     REQUIRE(flags, "null flags");
     if (nrows == 0) return CMF_OK;
-    const size_t es = precision == CMF_PREC_FP16 ? 2 : 4;
     cudaStream_t st = S(stream);
+    const int w16 = gram_tc_width(f);
+    if (kernel == CMF_GRAM_TC) {
+        REQUIRE(ws16, "CMF_GRAM_TC needs the ws16 shadow buffer");
+        int rc = factors_to_half_launch(fixed, ncols, f, ws16, w16, st);
+        if (rc) return rc;
+    }
     for (int64_t r0 = 0; r0 < nrows; r0 += ws_rows) {
         const int64_t nb = nrows - r0 < ws_rows ? nrows - r0 : ws_rows;
-        int rc = cmf_gram_assemble(indptr + r0, indices, nullptr, values, nb, fixed, ncols, f, lam,
-                                   weighted_reg, nullptr, precision, kernel, ws_a, a_stride, ws_b,
-                                   ws_nu, flags + 0, stream);
+        int rc = kernel == CMF_GRAM_TC
+                     ? cmf_gram_assemble_tc(indptr + r0, indices, values, nb, ws16, w16, f, lam,
+                                            weighted_reg, nullptr, precision, ws_a, a_stride, ws_b,
+                                            ws_nu, flags + 0, stream)
+                     : cmf_gram_assemble(indptr + r0, indices, nullptr, values, nb, fixed, ncols, f,
+                                         lam, weighted_reg, nullptr, precision, kernel, ws_a,
+                                         a_stride, ws_b, ws_nu, flags + 0, stream);
         if (rc) return rc;
         float *tgt = target + r0 * f;
         if (method == 0)
@@ -163,7 +198,6 @@ int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *
             rc = chol_launch(static_cast<const float *>(ws_a), a_stride, ws_b, ws_nu, nb, f,
                              accum == CMF_CG_FP64, tgt, nullptr, flags + 2, st);
         if (rc) return rc;
-        (void)es;
     }
     return CMF_OK;
 }

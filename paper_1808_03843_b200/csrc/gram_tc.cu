@@ -1,12 +1,334 @@
-// K1 tensor-core path (tcgen05 / TMEM): placeholder until the kernel lands.
-#include "common.cuh"
+// K1 + K2 on the 5th-generation tensor cores (tcgen05 + TMEM), CG route.
+//
+// Replaces gram._accumulate_chunk + _bias_chunk + pack_half (gram.py:149-220,
+// :132-146) for the approximate-computing path: the paper's get_hermitian is
+// a dense contraction per row, A_u = Theta_S^T Theta_S, so each row's gathered
+// factor rows are the K dimension of one M=128 x N x K MMA chain.
+//
+// Operand trick (tc_common.cuh): the gathered rows are staged ONCE per
+// K-chunk as an MN-major, 128-byte-swizzled UMMA operand and the SAME shared
+// buffer is passed as both A (M = 128 feature rows) and B (N = roundup16(f+2)
+// feature rows).  Rows f and f+1 of the operand carry the row's ratings
+// (fp16 hi + lo), so accumulator columns f, f+1 give b_u = sum_p r_p theta_p:
+// the bias rides along in the same MMAs (fp32 accumulation in TMEM).
+//
+// The fixed factor matrix is read from a binary16 shadow (cmf_factors_to_half,
+// row width W = roundup8(f+2) halves, zero padded) so every 16-byte chunk of
+// a gathered row is one cp.async: the gather needs no SIMT conversion, and
+// the shadow of X (Netflix: 100 MB) stays resident in the 126 MB L2.
+//
+// Warp roles (288 threads, 2 CTAs per SM, persistent over rows):
+//   warps 0-3  epilogue: tcgen05.ld the accumulator (thread i <-> TMEM lane i
+//              <-> matrix row i) into a square staging tile (+ lambda*n_u on the
+//              diagonal), then all 128 threads write the packed lower triangle
+//              to HBM through an offset table; b_u straight to global.
+//   warps 4-7  producers: cp.async gather of K-chunks (64 gathered rows) into
+//              a 4-stage ring, one warp per stage slot;
+//              cp.async.mbarrier.arrive.noinc completes full[s].
+//   warp 8     TMEM allocator + single-thread MMA issuer (kind::f16, fp32
+//              accumulate), tcgen05.commit -> empty[s] / tmem_full[b].
+// Two TMEM accumulators (2 x 128 columns) let the epilogue of row u overlap
+// the MMAs of row u+1.
+#include <type_traits>
+
+#include "tc_common.cuh"
 
 namespace cmf {
+namespace tc {
 
-int gram_tc_launch(const int64_t *, const int32_t *, const float *, const float *, int64_t,
-                   const float *, int, double, int, const float *, bool, void *, int64_t, float *,
-                   int64_t *, int32_t *, cudaStream_t) {
-    return set_error(CMF_EINVAL, "tensor-core Gram kernel not available in this build");
+constexpr int NUM_THREADS = 288;
+constexpr int EPI_THREADS = 128;
+
+struct Args {
+    GatherArgs gather;
+    int N;
+    double lam;
+    int weighted;
+    const float *base;
+    void *a_out;
+    int64_t a_stride;
+    float *b_out;
+    int64_t *nu_out;
+    int32_t *overflow;
+};
+
+__device__ __forceinline__ void bar_epi() { named_bar(1, EPI_THREADS); }
+
+// Packed-offset table: tab[k] = i*W + j for packed entry k = i*(i+1)/2 + j.
+// Built once per CTA; the epilogue copy-out walks the packed row with it.
+template <int NCH, bool HALF_OUT>
+__global__ void __launch_bounds__(NUM_THREADS, 2) gram_tc_kernel(Args g) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    constexpr int W = NCH * 8;
+    using SqT = typename std::conditional<HALF_OUT, __half, float>::type;
+    const GatherArgs &ga = g.gather;
+    const int f = ga.f;
+    const int64_t P = packed_size(f);
+    // layout: [stages (1024-aligned) | square staging (f x W, SqT) | offset table | barriers | tmem slot]
+    unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    unsigned char *stage_mem = smem;
+    SqT *sq = reinterpret_cast<SqT *>(smem + STAGES * STAGE_BYTES);
+    const size_t sq_bytes = ((static_cast<size_t>(f) * W * sizeof(SqT)) + 15) & ~static_cast<size_t>(15);
+    uint16_t *tab = reinterpret_cast<uint16_t *>(smem + STAGES * STAGE_BYTES + sq_bytes);
+    const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES + sq_bytes + tab_bytes);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + NUM_BARS);
+    Pipe pp{smem_u32(stage_mem), smem_u32(bars)};
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // zero the operand ring once: MN-blocks >= NCH (rows >= W) are never written again
+    for (int i = tid; i < STAGES * STAGE_BYTES / 16; i += NUM_THREADS)
+        reinterpret_cast<int4 *>(stage_mem)[i] = make_int4(0, 0, 0, 0);
+    for (int i = tid; i < f; i += NUM_THREADS) {
+        const int base = i * (i + 1) / 2;
+        for (int j = 0; j <= i; ++j) tab[base + j] = static_cast<uint16_t>(i * W + j);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(pp.full(s), 32);  // one producer warp per stage
+            mbar_init(pp.empty(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(pp.tfull(b), 1);
+            mbar_init(pp.tempty(b), EPI_THREADS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int64_t G = gridDim.x;
+    if (warp >= 4 && warp < 8) {
+        produce<NCH>(ga, pp, warp - 4, 4, lane, blockIdx.x, G);
+    } else if (warp == 8) {
+        if (lane == 0) issue_mma(ga, pp, tmem_base, g.N, blockIdx.x, G);
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ epilogue
+        // (1) thread i (= TMEM lane = matrix row) drains its accumulator row into
+        //     the square staging as fp16/fp32, then overwrites its diagonal with
+        //     fl(A_ii + lambda*n_u) (one rounding, as the reference); the bias is
+        //     read from accumulator columns f, f+1 in fp32.  (2) all 128 threads
+        //     walk the packed triangle with the offset table and write it
+        //     coalesced to HBM, four entries per step.
+        const int i = warp * 32 + lane;
+        const int nchunk = (g.N + 31) >> 5;
+        const int bias_cc = f >> 5, bias_cc1 = (f + 1) >> 5;
+        float ovf_max = 0.0f;
+        uint32_t rowc = 0;
+        SqT *sq_row = sq + static_cast<size_t>(i) * W;
+        for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
+            const int64_t p0 = ga.indptr[u], p1 = ga.indptr[u + 1];
+            const int64_t n_u = p1 - p0;
+            const float reg = g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
+                                         : __double2float_rn(g.lam);
+            float bias = 0.0f, diag = 0.0f;
+            if (n_u == 0) {
+                if (i < f)
+                    for (int j = 0; j < W; ++j) sq_row[j] = static_cast<SqT>(0.0f);
+            } else {
+                const int b = rowc & 1;
+                mbar_wait(pp.tfull(b), (rowc >> 1) & 1);
+                tc_fence_after();
+                const uint32_t tbase = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + b * 128;
+                for (int cc = 0; cc < nchunk; ++cc) {
+                    uint32_t v[32];
+                    tmem_ld32(tbase + cc * 32, v);
+                    tmem_ld_wait();
+                    const int c0 = cc * 32;
+                    if (cc == warp) {  // warp-uniform: this chunk holds every lane's diagonal
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            if (jj == lane) diag = __uint_as_float(v[jj]);
+                    }
+                    if (cc == bias_cc || cc == bias_cc1) {  // warp-uniform
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            if (c0 + jj == f || c0 + jj == f + 1) bias += __uint_as_float(v[jj]);
+                    }
+                    if (i < f) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if (c0 + 8 * q >= W) break;
+                            const float *x = reinterpret_cast<const float *>(v) + 8 * q;
+                            if (HALF_OUT) {
+                                __half2 h[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    h[e] = __floats2half2_rn(x[2 * e], x[2 * e + 1]);
+                                    ovf_max = fmaxf(ovf_max, fmaxf(fabsf(x[2 * e]), fabsf(x[2 * e + 1])));
+                                }
+                                *reinterpret_cast<uint4 *>(sq_row + c0 + 8 * q) = *reinterpret_cast<uint4 *>(h);
+                            } else {
+                                float4 *d = reinterpret_cast<float4 *>(sq_row + c0 + 8 * q);
+                                d[0] = make_float4(x[0], x[1], x[2], x[3]);
+                                d[1] = make_float4(x[4], x[5], x[6], x[7]);
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(pp.tempty(b));
+                ++rowc;
+            }
+            if (i < f) {
+                const float dv = diag + reg;
+                sq_row[i] = static_cast<SqT>(dv);
+                if (HALF_OUT) ovf_max = fmaxf(ovf_max, fabsf(dv));
+            }
+            if (g.b_out && i < f) g.b_out[u * f + i] = bias;
+            if (tid == 0 && g.nu_out) g.nu_out[u] = n_u;
+            bar_epi();
+            // packed copy-out: entries k..k+3 per step (k % 4 == 0)
+            const size_t row_off = static_cast<size_t>(u) * g.a_stride;
+            if (!g.base) {
+                for (int64_t k = 4 * tid; k < P; k += 4 * EPI_THREADS) {
+                    const uint2 o = *reinterpret_cast<const uint2 *>(tab + k);
+                    const int64_t nk = P - k;
+                    SqT e0 = sq[o.x & 0xFFFF];
+                    SqT e1 = nk > 1 ? sq[o.x >> 16] : SqT(0.0f);
+                    SqT e2 = nk > 2 ? sq[o.y & 0xFFFF] : SqT(0.0f);
+                    SqT e3 = nk > 3 ? sq[o.y >> 16] : SqT(0.0f);
+                    SqT *dst = static_cast<SqT *>(g.a_out) + row_off + k;
+                    if (nk >= 4 && (reinterpret_cast<uintptr_t>(dst) & (4 * sizeof(SqT) - 1)) == 0) {
+                        if (HALF_OUT) {
+                            __half2 a = __halves2half2(e0, e1), c = __halves2half2(e2, e3);
+                            uint2 w;
+                            w.x = *reinterpret_cast<uint32_t *>(&a);
+                            w.y = *reinterpret_cast<uint32_t *>(&c);
+                            *reinterpret_cast<uint2 *>(dst) = w;
+                        } else {
+                            *reinterpret_cast<float4 *>(dst) = make_float4(e0, e1, e2, e3);
+                        }
+                    } else {
+                        dst[0] = e0;
+                        if (nk > 1) dst[1] = e1;
+                        if (nk > 2) dst[2] = e2;
+                        if (nk > 3) dst[3] = e3;
+                    }
+                }
+            } else {  // implicit-style base matrix: add in fp32, round once more
+                for (int64_t k = tid; k < P; k += EPI_THREADS) {
+                    const float a = static_cast<float>(sq[tab[k]]) + g.base[k];
+                    static_cast<SqT *>(g.a_out)[row_off + k] = static_cast<SqT>(a);
+                    if (HALF_OUT) ovf_max = fmaxf(ovf_max, fabsf(a));
+                }
+            }
+            bar_epi();  // staging free for the next row
+        }
+        if (HALF_OUT && ovf_max >= 65520.0f && isfinite(ovf_max) && g.overflow) atomicOr(g.overflow, 1);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
+// fp32 (rows, f) -> binary16 (rows, W), zero padded, RNE.
+__global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __half *out, int W) {
+    const int64_t n = rows * W;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
+        const int64_t r = e / W;
+        const int c = static_cast<int>(e - r * W);
+        out[e] = c < f ? __float2half_rn(x[r * f + c]) : __float2half_rn(0.0f);
+    }
+}
+
+}  // namespace tc
+
+int gram_tc_width(int f) { return ((f + 2 + 7) / 8) * 8; }
+
+int factors_to_half_launch(const float *x, int64_t rows, int f, void *out, int W, cudaStream_t st) {
+    if (rows == 0) return CMF_OK;
+    int64_t blocks = (rows * W + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    tc::factors_to_half_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, rows, f,
+                                                                             static_cast<__half *>(out), W);
+    return check_launch("factors_to_half_kernel");
+}
+
+template <int NCH, bool H>
+static int launch_nch(const tc::Args &g, size_t smem, int64_t nrows, cudaStream_t st) {
+    auto k = tc::gram_tc_kernel<NCH, H>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return set_error(CMF_ECUDA, "gram_tc smem attr: %s", cudaGetErrorString(e));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    // two CTAs per SM when their shared memory fits (TMEM: 2 x 256 columns per SM)
+    per_sm = (2 * (smem + 1024) <= 227 * 1024) ? 2 : 1;
+    int64_t grid = static_cast<int64_t>(per_sm) * sms;
+    if (grid > nrows) grid = nrows;
+    k<<<static_cast<unsigned>(grid), tc::NUM_THREADS, smem, st>>>(g);
+    return check_launch("gram_tc_kernel");
+}
+
+template <bool H>
+static int dispatch_nch(int nch, const tc::Args &g, size_t smem, int64_t nrows, cudaStream_t st) {
+    switch (nch) {
+        case 1: return launch_nch<1, H>(g, smem, nrows, st);
+        case 2: return launch_nch<2, H>(g, smem, nrows, st);
+        case 3: return launch_nch<3, H>(g, smem, nrows, st);
+        case 4: return launch_nch<4, H>(g, smem, nrows, st);
+        case 5: return launch_nch<5, H>(g, smem, nrows, st);
+        case 6: return launch_nch<6, H>(g, smem, nrows, st);
+        case 7: return launch_nch<7, H>(g, smem, nrows, st);
+        case 8: return launch_nch<8, H>(g, smem, nrows, st);
+        case 9: return launch_nch<9, H>(g, smem, nrows, st);
+        case 10: return launch_nch<10, H>(g, smem, nrows, st);
+        case 11: return launch_nch<11, H>(g, smem, nrows, st);
+        case 12: return launch_nch<12, H>(g, smem, nrows, st);
+        case 13: return launch_nch<13, H>(g, smem, nrows, st);
+        case 14: return launch_nch<14, H>(g, smem, nrows, st);
+        case 15: return launch_nch<15, H>(g, smem, nrows, st);
+        default: return launch_nch<16, H>(g, smem, nrows, st);
+    }
+}
+
+int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
+                   const void *fixed16, int W, int f, double lam, int weighted, const float *base, bool half,
+                   void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out, int32_t *overflow,
+                   cudaStream_t st) {
+    if (nrows == 0) return CMF_OK;
+    if (f + 2 > tc::M)
+        return set_error(CMF_EINVAL, "tensor-core Gram supports f <= %d (got %d)", tc::M - 2, f);
+    if (W != gram_tc_width(f)) return set_error(CMF_EINVAL, "fixed16 width must be %d", gram_tc_width(f));
+    const int esz = half ? 2 : 4;
+    if ((a_stride % 2) != 0 || (reinterpret_cast<uintptr_t>(a_out) & 15) != 0)
+        return set_error(CMF_EINVAL, "tensor-core Gram needs an even a_stride and a 16-byte aligned a_out");
+    if ((reinterpret_cast<uintptr_t>(fixed16) & 15) != 0)
+        return set_error(CMF_EINVAL, "fixed16 must be 16-byte aligned");
+    tc::Args g{};
+    g.gather.indptr = indptr;
+    g.gather.indices = indices;
+    g.gather.values = values;
+    g.gather.fixed16 = static_cast<const __half *>(fixed16);
+    g.gather.nrows = nrows;
+    g.gather.f = f;
+    g.N = ((f + 2 + 15) / 16) * 16;
+    g.lam = lam;
+    g.weighted = weighted;
+    g.base = base;
+    g.a_out = a_out;
+    g.a_stride = a_stride;
+    g.b_out = b_out;
+    g.nu_out = nu_out;
+    g.overflow = overflow;
+    const int64_t P = packed_size(f);
+    const size_t sq_bytes = ((static_cast<size_t>(f) * W * esz) + 15) & ~static_cast<size_t>(15);
+    const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
+    const size_t smem = 1024 + tc::STAGES * tc::STAGE_BYTES + sq_bytes + tab_bytes + tc::NUM_BARS * 8 + 16;
+    const int nch = W / 8;
+    return half ? dispatch_nch<true>(nch, g, smem, nrows, st) : dispatch_nch<false>(nch, g, smem, nrows, st);
 }
 
 }  // namespace cmf

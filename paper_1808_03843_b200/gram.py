@@ -189,17 +189,33 @@ def assemble_side(view: RowView, theta, lam: float, cfg: TileConfig | None = Non
     aw = None if a_weights is None else nat.to_dev(a_weights, torch.float32, dev)
     bw = values if b_weights is None else nat.to_dev(b_weights, torch.float32, dev)
     nrows = int(view.nrows)
-    a_out = torch.empty((nrows, P), dtype=torch.float16 if precision == "fp16" else torch.float32,
-                        device=dev)
+    dt = torch.float16 if precision == "fp16" else torch.float32
     b_out = torch.empty((nrows, f), dtype=torch.float32, device=dev)
     nu = torch.empty(nrows, dtype=torch.int64, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    nat.call("cmf_gram_assemble", nat.ptr(indptr), nat.ptr(indices), nat.ptr(aw), nat.ptr(bw),
-             nrows, nat.ptr(th), th.shape[0], f, float(lam), int(bool(weighted_reg)), nat.ptr(base),
-             nat.PREC[precision], nat.GRAM_KERNELS[kernel], nat.ptr(a_out), P, nat.ptr(b_out),
-             nat.ptr(nu), nat.ptr(flag), nat.stream_ptr())
+    if kernel == "tc":
+        if aw is not None:
+            raise DataError("the tensor-core Gram kernel does not take a_weights")
+        stride = (P + 7) // 8 * 8  # 16-byte rows for the bulk store
+        a_full = torch.empty((nrows, stride), dtype=dt, device=dev)
+        w16 = nat.tc_width(f)
+        shadow = torch.empty((th.shape[0], w16), dtype=torch.float16, device=dev)
+        nat.call("cmf_factors_to_half", nat.ptr(th), th.shape[0], f, nat.ptr(shadow), w16,
+                 nat.stream_ptr())
+        nat.call("cmf_gram_assemble_tc", nat.ptr(indptr), nat.ptr(indices), nat.ptr(bw), nrows,
+                 nat.ptr(shadow), w16, f, float(lam), int(bool(weighted_reg)), nat.ptr(base),
+                 nat.PREC[precision], nat.ptr(a_full), stride, nat.ptr(b_out), nat.ptr(nu),
+                 nat.ptr(flag), nat.stream_ptr())
+        a_out = a_full[:, :P]
+    else:
+        a_out = torch.empty((nrows, P), dtype=dt, device=dev)
+        nat.call("cmf_gram_assemble", nat.ptr(indptr), nat.ptr(indices), nat.ptr(aw),
+                 nat.ptr(bw), nrows, nat.ptr(th), th.shape[0], f, float(lam),
+                 int(bool(weighted_reg)), nat.ptr(base), nat.PREC[precision],
+                 nat.GRAM_KERNELS[kernel], nat.ptr(a_out), P, nat.ptr(b_out), nat.ptr(nu),
+                 nat.ptr(flag), nat.stream_ptr())
     ev1.record()
     if int(flag.item()):
         raise NumericalError("Gram entries overflow binary16 range (+-65504); "

@@ -69,13 +69,18 @@ def _singular_error(rows):
     return SingularSystemError(msg, rows=rows)
 
 
+def _row_stride(a: torch.Tensor) -> int:
+    # a size-1 leading dim may carry any stride (numpy's a[None, :] has 0)
+    return a.stride(0) if a.shape[0] > 1 else a.shape[1]
+
+
 def cholesky_device(a: torch.Tensor, b: torch.Tensor, nu=None, accum: str = "fp32",
                     out: torch.Tensor | None = None, raise_singular: bool = True):
     """Device-level K4 on (N, stride>=P) float32 packed systems."""
     n_sys, f = b.shape
     out = torch.empty_like(b) if out is None else out
     info = torch.zeros(n_sys, dtype=torch.int32, device=b.device)
-    nat.call("cmf_batch_cholesky", nat.ptr(a), a.stride(0), nat.ptr(b), nat.ptr(nu), n_sys, f,
+    nat.call("cmf_batch_cholesky", nat.ptr(a), _row_stride(a), nat.ptr(b), nat.ptr(nu), n_sys, f,
              nat.ACCUM[accum], nat.ptr(out), nat.ptr(info), None, nat.stream_ptr())
     if raise_singular:
         bad = torch.nonzero(info).flatten()
@@ -92,7 +97,7 @@ def cg_device(a: torch.Tensor, b: torch.Tensor, x0: torch.Tensor, f_s: int, cg_t
     iters = torch.zeros(n_sys, dtype=torch.int32, device=b.device)
     broke = torch.zeros(n_sys, dtype=torch.int32, device=b.device)
     nat.call("cmf_batch_cg", nat.ptr(a), nat.PREC["fp16" if a.dtype == torch.float16 else "fp32"],
-             a.stride(0), nat.ptr(b), nat.ptr(x0), nat.ptr(eps), float(cg_tol), nat.ptr(nu), n_sys,
+             _row_stride(a), nat.ptr(b), nat.ptr(x0), nat.ptr(eps), float(cg_tol), nat.ptr(nu), n_sys,
              f, int(f_s), nat.ACCUM[accum], nat.ptr(out), nat.ptr(iters), nat.ptr(broke), None,
              nat.stream_ptr())
     return out, iters, broke

@@ -1,0 +1,102 @@
+"""Tensor-core Gram (tcgen05 kind::f16, TMEM accumulators) on the GPU.
+
+The kernel rounds the fixed factors to binary16 (RNE) and the ratings to an
+fp16 hi+lo pair, multiplies exactly and accumulates in fp32.  So it is checked
+tightly (1e-5 relative Frobenius per row) against a float64 Gram of the
+SAME fp16-rounded operands -- which pins the operand layout, the rating rows
+and the packed epilogue exactly -- and loosely against the fp32 reference
+(the input rounding, ~2^-11)."""
+
+import numpy as np
+import pytest
+
+import paper_1808_03843_b200 as cmfb
+from paper_1808_03843_b200.data import RowView
+
+pytestmark = pytest.mark.gpu
+
+
+def _instance(m, n, f, degs, seed):
+    rng = np.random.default_rng(seed)
+    rows = [np.sort(rng.choice(n, size=min(d, n), replace=False)) for d in degs]
+    indptr = np.zeros(m + 1, np.int64)
+    indptr[1:] = np.cumsum([len(r) for r in rows])
+    indices = np.concatenate(rows).astype(np.int32) if indptr[-1] else np.zeros(0, np.int32)
+    values = rng.standard_normal(indices.shape[0]).astype(np.float32)
+    theta = (rng.random((n, f), dtype=np.float32) - 0.5)
+    return RowView(indptr, indices, values, m, n), theta
+
+
+def _f64_reference(view, theta, lam, weighted=True):
+    t16 = theta.astype(np.float16).astype(np.float64)
+    f = theta.shape[1]
+    out_a, out_b = [], []
+    for u in range(view.nrows):
+        lo, hi = view.indptr[u], view.indptr[u + 1]
+        sel = t16[view.indices[lo:hi]]
+        r = view.values[lo:hi]
+        r_hi = r.astype(np.float16).astype(np.float64)
+        r_lo = (r - r_hi.astype(np.float32)).astype(np.float16).astype(np.float64)
+        a = sel.T @ sel + (lam * (hi - lo) if weighted else lam) * np.eye(f)
+        out_a.append(a[np.tril_indices(f)])
+        out_b.append(sel.T @ (r_hi + r_lo))
+    return np.array(out_a), np.array(out_b)
+
+
+@pytest.mark.parametrize("f,degs", [
+    (100, [206, 0, 1, 63, 64, 65, 300, 5571]),
+    (32, [166, 270, 0, 17, 128]),
+    (8, [3, 40, 0]),
+    (1, [5, 0, 9]),
+    (63, [100, 2000, 64]),
+    (126, [129, 7]),
+])
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+def test_tc_gram_matches_fp16_operand_reference(cuda_device, f, degs, precision):
+    n = max(max(degs) + 10, 64)
+    view, theta = _instance(len(degs), n, f, degs, seed=f + len(degs))
+    gb, _ = cmfb.assemble_side(view, theta, 0.05, precision=precision, kernel="tc")
+    a_ref, b_ref = _f64_reference(view, theta, 0.05)
+    a = np.asarray(gb.a_lower, dtype=np.float64)
+    for u in range(view.nrows):
+        # fp16 storage rounds the result; fp32 keeps the tensor core's accumulation order
+        tol = 1e-3 if precision == "fp16" else 5e-5
+        da = np.linalg.norm(a[u] - a_ref[u]) / max(np.linalg.norm(a_ref[u]), 1e-30)
+        assert da <= tol or np.abs(a[u] - a_ref[u]).max() < 1e-7, (u, da)
+        if degs[u]:
+            db = np.linalg.norm(gb.b[u] - b_ref[u]) / max(np.linalg.norm(b_ref[u]), 1e-30)
+            assert db <= 1e-5, (u, db)
+        else:
+            assert np.array_equal(gb.b[u], np.zeros(f, np.float32))
+    assert np.array_equal(gb.n_u, np.array(degs, np.int64).clip(max=n))
+
+
+def test_tc_gram_close_to_reference_fp32(golden, cuda_device):
+    g = golden("gram_cases")
+    for ci in range(int(g["ncases"])):
+        p = f"c{ci}_"
+        m, n, f = (int(v) for v in g[p + "meta"])
+        if f > 126:
+            continue
+        view = RowView(g[p + "row_ptr"], g[p + "col_idx"], g[p + "csr_val"], m, n)
+        theta = g[p + "theta_n"]
+        gb, _ = cmfb.assemble_side(view, theta, 0.05, kernel="tc")
+        ref = g[p + "x_fp32_1_a"].astype(np.float64)
+        for u in range(m):
+            d = np.linalg.norm(gb.a_lower[u] - ref[u]) / max(np.linalg.norm(ref[u]), 1e-30)
+            assert d < 2e-3, (p, u, d)
+
+
+def test_tc_train_rmse_trajectory_ml1m(golden, cuda_device):
+    """CG-fp16 with the tensor-core Gram: RMSE trajectory within 1e-3 of the reference."""
+    g = golden("train_ml1m")
+    m, n, nnz, f = (int(v) for v in g["meta"])
+    t, _ = cmfb.gen_synthetic(m, n, f, round(nnz / 0.9) / (m * n), 0.1, 0)
+    tr, te = cmfb.split_holdout(t, 0.1, 1)
+    sr = cmfb.build(tr, m, n)
+    for solver, prec in (("cg16", "fp16"), ("cg32", "fp32")):
+        cfg = cmfb.AlsConfig(f=f, lam=0.05, epochs=10, gram_kernel="tc",
+                             solver=cmfb.SolverConfig("cg", precision=prec))
+        _, _, rep = cmfb.train(sr, te, cfg)
+        traj = np.array(rep.rmse_trajectory())
+        assert np.abs(traj - g[solver + "_rmse"]).max() < 1e-3, (solver, traj)

@@ -55,7 +55,7 @@ def test_cg_breakdown_and_known_answers(golden, cuda_device):
                              cmfb.SolverConfig("cg", 3, 0.0, accum=accum))
         assert r.breakdowns == 1
         assert np.array_equal(r.x[1], g["bd_x0"][1])
-        assert np.allclose(r.x, g["bd_x"], rtol=1e-6)
+        assert np.allclose(r.x, g["bd_x"], rtol=1e-6 if accum == "fp64" else 1e-5)
     s = cmfb.GramSystem(2, cmfb.pack_lower(np.array([[4.0, 1.0], [1.0, 3.0]])),
                         np.array([1.0, 2.0], np.float32), 1)
     x = cmfb.cg_solve(s, np.array([2.0, 1.0], np.float32), f_s=2, eps=0.0)
