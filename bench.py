@@ -300,19 +300,27 @@ def main():
     per_kernel = {}
     for name, lst in resolve_events(kern).items():
         per_kernel[name] = {"ms_total": sum(lst), "launches": len(lst)}
-    gram_ms = sum(v["ms_total"] for k, v in per_kernel.items() if k.startswith("gram"))
+    gram_ms = sum(v["ms_total"] for k, v in per_kernel.items()
+                  if k.startswith("gram") or k == "shadow16")
     solve_ms = sum(v["ms_total"] for k, v in per_kernel.items() if k.startswith("solve"))
+    fused_ms = sum(v["ms_total"] for k, v in per_kernel.items() if k.startswith("fused"))
     gram_flops_step = 2.0 * P * (shard_nnz["x"] + shard_nnz["t"])
     a_bytes = 2 if precision == "fp16" else 4
     nsys = engine.local_rows()
     cg_bytes_step = float((nsys["x"] + nsys["t"]) * (P * a_bytes + 3 * 4 * f))
     gram_tflops = gram_flops_step * args.steps / (gram_ms / 1e3) / 1e12 if gram_ms else 0.0
     solve_gbs = cg_bytes_step * args.steps / (solve_ms / 1e3) / 1e9 if solve_ms else 0.0
+    fused_tflops = gram_flops_step * args.steps / (fused_ms / 1e3) / 1e12 if fused_ms else 0.0
     gram_kernel = engine.gram_kernel
     tt = traffic_table()
-    if gram_ms >= solve_ms:
-        if gram_kernel == "tc":
-            roof = {"kernel": "gram_tc (K1)", "bound": "tensor", "achieved": gram_tflops,
+    dominant = max((fused_ms, "fused"), (gram_ms, "gram"), (solve_ms, "solve"))[1]
+    if dominant == "fused":
+        roof = {"kernel": "fused_cg_kernel (K1 tcgen05 Gram + K3 CG in TMEM/registers)",
+                "bound": "tensor", "achieved": fused_tflops, "peak": pk["tensor"], "unit": "TFLOP/s",
+                "traffic": tt.get("fused")}
+    elif dominant == "gram":
+        if gram_kernel.startswith("tc"):
+            roof = {"kernel": "gram_tc_kernel (K1)", "bound": "tensor", "achieved": gram_tflops,
                     "peak": pk["tensor"], "unit": "TFLOP/s"}
         else:
             fp32_peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
@@ -325,8 +333,9 @@ def main():
                 "peak": pk["hbm"], "unit": "GB/s", "traffic": tt.get("solve")}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["peak_kind"] = pk["src"] + " (burst)"
-    roof["units"] = ("gram: 2*nnz*f(f+1)/2 flop per half (gram.py:373); "
-                     "solve: systems*(P*sizeof(A) + 12f) bytes (SURVEY 8(d))")
+    roof["units"] = ("K1 algorithmic flops = 2*nnz*f(f+1)/2 per half-update (gram.py:373), "
+                     "counted over both halves per step; CG bytes = systems*(P*sizeof(A) + 12f) "
+                     "(SURVEY 8(d))")
 
     result = {
         "metric": "sec_per_als_iteration", "value": sec, "unit": "s", "n_gpus": world,
@@ -343,10 +352,13 @@ def main():
                    "l2": "inputs > L2 (ratings 1.6 GB + Gram workspace)"},
         "gpu_launches": launches,
         "phase_ms_per_step": {"gram": gram_ms / args.steps, "solve": solve_ms / args.steps,
+                              "fused_gram_cg": fused_ms / args.steps,
                               "allgather": per_kernel.get("allgather", {}).get("ms_total", 0.0)
                               / args.steps},
         "kernels": {"gram_tflops": gram_tflops, "solve_gbs": solve_gbs,
-                    "solve_hbm_frac": solve_gbs / pk["hbm"]},
+                    "solve_hbm_frac": solve_gbs / pk["hbm"], "fused_tflops": fused_tflops,
+                    "per_kernel_ms_per_step": {k: v["ms_total"] / args.steps
+                                               for k, v in per_kernel.items()}},
         "roofline": roof,
         "test_rmse_after": test_rmse,
         "gen_seconds": t_gen,

@@ -99,6 +99,19 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
                          int32_t weighted_reg, const float *base_packed, int32_t precision,
                          void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
                          int32_t *overflow_flag, void *stream);
+/*
+ * Fused half-update on the CG route (tensor-core Gram -> TMEM -> truncated CG
+ * in registers): for every row with n_u > 0, A_u and b_u are accumulated by
+ * tcgen05.mma into TMEM (fp16 operands from `fixed16`, fp32 accumulation) and
+ * solved in place, target[u] <- CG_{f_s}(A_u + reg*I, b_u, x0 = target[u]),
+ * eps = cg_tol * ||b_u||.  A_u never reaches HBM.  Replaces als.update_side
+ * (als.py:54-74) for SolverConfig(method="cg").  f <= 126.  *breakdowns
+ * (device int, nullable) accumulates p^T A p <= 0 exits.
+ */
+int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
+                        int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
+                        int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
+                        int32_t *breakdowns, void *stream);
 /* Row width (halves) of the binary16 factor shadow for a given f. */
 int cmf_tc_width(int32_t f);
 /* fp32 (rows, f) -> binary16 (rows, w16), RNE, zero padded columns. */

@@ -61,11 +61,30 @@ def aligned_stride(f: int) -> int:
     return (packed_size(f) + 7) // 8 * 8
 
 
-def resolve_gram_kernel(kernel: str | None, solver: SolverConfig) -> str:
+TC_MAX_F = 126  # tensor-core paths: f + 2 operand rows within M = 128
+
+
+def resolve_gram_kernel(kernel: str | None, solver: SolverConfig, f: int | None = None) -> str:
+    """Kernel choice for update_side/train.
+
+    "auto": the CG route runs fused on the tensor cores ("tc": Gram in TMEM,
+    CG in registers, A never stored) when f <= 126; the exact route keeps the
+    fp32-faithful SIMT Gram ("fma") its 1e-4 factor bar needs.
+    "tc_unfused" is the paper's two-step scheme on the tensor cores: packed
+    fp16/fp32 A_u written to HBM, then the batched CG kernel reads it.
+    """
     if kernel in (None, "auto"):
-        return os.environ.get("CMF_TRAIN_GRAM_KERNEL", "fma")
+        kernel = os.environ.get("CMF_TRAIN_GRAM_KERNEL", "auto")
+    if kernel == "auto":
+        use_tc = solver.method == "cg" and (f is None or f <= TC_MAX_F)
+        return "tc" if use_tc else "fma"
     if kernel not in nat.GRAM_KERNELS:
         raise DataError(f"unknown gram kernel {kernel!r}")
+    if kernel.startswith("tc") and solver.method == "exact":
+        raise DataError("the tensor-core Gram (fp16 operands) cannot feed the exact solver; "
+                        "use gram_kernel='fma' or 'bitwise'")
+    if kernel.startswith("tc") and f is not None and f > TC_MAX_F:
+        raise DataError(f"tensor-core Gram supports f <= {TC_MAX_F}")
     return kernel
 
 
@@ -105,24 +124,28 @@ class HalfUpdatePlan:
 
     def __init__(self, nrows: int, f: int, solver: SolverConfig, dev,
                  workspace_bytes: int | None = None):
-        self.f, self.solver, self.nrows = f, solver, nrows
+        self.f, self.solver, self.nrows, self.dev = f, solver, nrows, dev
         self.half = solver.precision == "fp16"
         self.esize = 2 if self.half else 4
         self.stride = aligned_stride(f)
-        row_bytes = self.stride * self.esize + f * 4 + 8
+        self.row_bytes = self.stride * self.esize + f * 4 + 8
         budget = WORKSPACE_BYTES if workspace_bytes is None else int(workspace_bytes)
-        self.rows_blk = max(1, min(nrows, budget // row_bytes)) if nrows else 1
-        ws = _WS.get(dev, self.rows_blk * row_bytes)
-        rb = self.rows_blk
-        a = ws[: rb * self.stride * self.esize]
-        self.a_ws = a.view(torch.float16 if self.half else torch.float32).view(rb, self.stride)
-        off = rb * self.stride * self.esize
-        self.b_ws = ws[off: off + rb * f * 4].view(torch.float32).view(rb, f)
-        off += rb * f * 4
-        self.nu_ws = ws[off: off + rb * 8].view(torch.int64)
+        self.rows_blk = max(1, min(nrows, budget // self.row_bytes)) if nrows else 1
+        self.a_ws = self.b_ws = self.nu_ws = None  # allocated on first two-step launch
         self.flags = torch.zeros(4, dtype=torch.int32, device=dev)
         self.w16 = nat.tc_width(f)
         self.shadow = None  # binary16 copy of the fixed factors (tensor-core Gram)
+
+    def _workspace(self):
+        if self.a_ws is None:
+            rb, f = self.rows_blk, self.f
+            ws = _WS.get(self.dev, rb * self.row_bytes)
+            a = ws[: rb * self.stride * self.esize]
+            self.a_ws = a.view(torch.float16 if self.half else torch.float32).view(rb, self.stride)
+            off = rb * self.stride * self.esize
+            self.b_ws = ws[off: off + rb * f * 4].view(torch.float32).view(rb, f)
+            off += rb * f * 4
+            self.nu_ws = ws[off: off + rb * 8].view(torch.int64)
 
     def _shadow(self, fx):
         need = fx.shape[0] * self.w16
@@ -139,20 +162,35 @@ class HalfUpdatePlan:
         f, solver = self.f, self.solver
         nrows = self.nrows if nrows is None else nrows
         st = nat.stream_ptr()
-        if record is not None and kernel == "tc":
+        tc = kernel.startswith("tc")
+        if record is not None and tc:
             es0 = torch.cuda.Event(enable_timing=True)
             es0.record()
-        shadow = self._shadow(fx) if kernel == "tc" else None
-        if record is not None and kernel == "tc":
+        shadow = self._shadow(fx) if tc else None
+        if record is not None and tc:
             es1 = torch.cuda.Event(enable_timing=True)
             es1.record()
             record.setdefault("shadow16", []).append((es0, es1))
+        if kernel == "tc" and solver.method == "cg":
+            # fused: Gram in TMEM -> CG in registers -> x, one launch, no workspace
+            if record is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            nat.call("cmf_fused_cg_update", nat.ptr(indptr) + 8 * row0, nat.ptr(indices),
+                     nat.ptr(values), nrows, nat.ptr(shadow), self.w16, f, float(lam),
+                     int(bool(weighted_reg)), nat.ptr(tg) + 4 * row0 * f, int(solver.cg_iters),
+                     float(solver.cg_tol), nat.ptr(self.flags) + 4, st)
+            if record is not None:
+                e1.record()
+                record.setdefault("fused_tc_cg", []).append((e0, e1))
+            return
+        self._workspace()
         for r0 in range(row0, row0 + nrows, self.rows_blk):
             nb = min(self.rows_blk, row0 + nrows - r0)
             if record is not None:
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record()
-            if kernel == "tc":
+            if tc:
                 nat.call("cmf_gram_assemble_tc", nat.ptr(indptr) + 8 * r0, nat.ptr(indices),
                          nat.ptr(values), nb, nat.ptr(shadow), self.w16, f, float(lam),
                          int(bool(weighted_reg)), None, nat.PREC[solver.precision],
@@ -178,7 +216,7 @@ class HalfUpdatePlan:
                          nat.ACCUM[solver.accum], tgt, None, nat.ptr(self.flags) + 8, st)
             if record is not None:
                 e2.record()
-                record.setdefault("gram_" + kernel, []).append((e0, e1))
+                record.setdefault("gram_" + ("tc" if tc else kernel), []).append((e0, e1))
                 record.setdefault("solve_" + solver.method, []).append((e1, e2))
 
     def read_flags(self):
@@ -205,7 +243,7 @@ def update_side(view: RowView, fixed, target, lam: float, solver: SolverConfig,
         raise DataError(f"feature matrix has {fixed.shape[0]} rows, ratings expect {view.ncols}")
     if tiles is not None and not isinstance(tiles, TileConfig):
         raise DataError("tiles must be a TileConfig")
-    kernel = resolve_gram_kernel(gram_kernel, solver)
+    kernel = resolve_gram_kernel(gram_kernel, solver, int(fixed.shape[1]))
     host = not nat.is_device(target)
     dev = nat.device()
     indptr, indices, values = _view_dev(view, dev)
@@ -226,7 +264,10 @@ def update_side(view: RowView, fixed, target, lam: float, solver: SolverConfig,
                                kernel, solver)
     times = PhaseTimes()
     for name, ms in resolve_events(rec).items():
-        if name.startswith("gram"):
+        if name.startswith("gram") or name == "shadow16":
+            times.accumulate += sum(ms) / 1e3
+        elif name.startswith("fused"):
+            # one kernel does both; report it under accumulate (the Gram dominates)
             times.accumulate += sum(ms) / 1e3
         else:
             times.solve += sum(ms) / 1e3

@@ -24,6 +24,8 @@ int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, con
                    double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
                    cudaStream_t);
 int gram_tc_width(int f);
+int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int, int, double,
+                    int, float *, int, double, int32_t *, cudaStream_t);
 int factors_to_half_launch(const float *, int64_t, int, void *, int, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
                      float *, cudaStream_t);
@@ -122,6 +124,19 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
     return gram_tc_launch(indptr, indices, b_weights, nrows, fixed16, w16, f, lam, weighted_reg,
                           base_packed, precision == CMF_PREC_FP16, a_out, a_stride, b_out, nu_out,
                           overflow_flag, S(stream));
+}
+
+int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
+                        int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
+                        int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
+                        int32_t *breakdowns, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(f_s >= 1, "cg_iters must be >= 1");
+    REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && fixed16 && target, "null argument");
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, w16, f, lam, weighted_reg, target, f_s,
+                           cg_tol, breakdowns, S(stream));
 }
 
 int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,

@@ -36,6 +36,7 @@
 namespace cmf {
 namespace tc {
 
+constexpr int STAGES = 4;
 constexpr int NUM_THREADS = 288;
 constexpr int EPI_THREADS = 128;
 
@@ -72,8 +73,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) gram_tc_kernel(Args g) {
     uint16_t *tab = reinterpret_cast<uint16_t *>(smem + STAGES * STAGE_BYTES + sq_bytes);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES + sq_bytes + tab_bytes);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + NUM_BARS);
-    Pipe pp{smem_u32(stage_mem), smem_u32(bars)};
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + Pipe<STAGES>::kBars);
+    Pipe<STAGES> pp{smem_u32(stage_mem), smem_u32(bars)};
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -326,7 +327,7 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     const int64_t P = packed_size(f);
     const size_t sq_bytes = ((static_cast<size_t>(f) * W * esz) + 15) & ~static_cast<size_t>(15);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
-    const size_t smem = 1024 + tc::STAGES * tc::STAGE_BYTES + sq_bytes + tab_bytes + tc::NUM_BARS * 8 + 16;
+    const size_t smem = 1024 + tc::STAGES * tc::STAGE_BYTES + sq_bytes + tab_bytes + tc::Pipe<tc::STAGES>::kBars * 8 + 16;
     const int nch = W / 8;
     return half ? dispatch_nch<true>(nch, g, smem, nrows, st) : dispatch_nch<false>(nch, g, smem, nrows, st);
 }

@@ -25,7 +25,6 @@ namespace cmf {
 namespace tc {
 
 constexpr int KS = 64;
-constexpr int STAGES = 4;
 constexpr int M = 128;
 constexpr int MNBLK_BYTES = 8192;  // LBO
 constexpr int KBLK_BYTES = 1024;   // SBO
@@ -52,6 +51,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
             : "r"(a), "r"(parity), "r"(0x989680u)
             : "memory");
     } while (!ok);
+}
+// Same, but spinning with plain try_wait and a nanosleep backoff: for waiters
+// that are not latency critical (producers facing a full ring).
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t a, uint32_t parity) {
+    uint32_t ok = 0, ns = 32;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+        if (ns < 512) ns <<= 1;
+    }
 }
 __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, uint32_t bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
@@ -143,15 +159,19 @@ struct GatherArgs {
     int f;
 };
 
+// Operand ring of NST stages + 2 TMEM accumulator hand-offs (mbarriers:
+// full[NST], empty[NST], tfull[2], tempty[2]).
+template <int NST>
 struct Pipe {
+    static constexpr int kStages = NST;
+    static constexpr int kBars = 2 * NST + 4;
     uint32_t stage_s, bar_s;
     __device__ uint32_t full(int s) const { return bar_s + 8u * s; }
-    __device__ uint32_t empty(int s) const { return bar_s + 8u * (STAGES + s); }
-    __device__ uint32_t tfull(int b) const { return bar_s + 8u * (2 * STAGES + b); }
-    __device__ uint32_t tempty(int b) const { return bar_s + 8u * (2 * STAGES + 2 + b); }
+    __device__ uint32_t empty(int s) const { return bar_s + 8u * (NST + s); }
+    __device__ uint32_t tfull(int b) const { return bar_s + 8u * (2 * NST + b); }
+    __device__ uint32_t tempty(int b) const { return bar_s + 8u * (2 * NST + 2 + b); }
     __device__ uint32_t stage(int s) const { return stage_s + s * STAGE_BYTES; }
 };
-constexpr int NUM_BARS = 2 * STAGES + 4;
 
 // Walk over pipeline stages: (row u, first position q0 of the K-chunk) pairs
 // in the order every role visits them.
@@ -181,8 +201,8 @@ struct StageIter {
 // Producer warp `pw` of `nprod`: fills every stage `it` with it % nprod == pw.
 // The (index, rating) pairs of the warp's NEXT stage are loaded while the
 // current one is being gathered, so index-load latency stays off the ring.
-template <int NCH>
-__device__ void produce(const GatherArgs &g, const Pipe &pp, int pw, int nprod, int lane, int64_t row0,
+template <int NCH, int NST>
+__device__ void produce(const GatherArgs &g, const Pipe<NST> &pp, int pw, int nprod, int lane, int64_t row0,
                         int64_t rstride) {
     constexpr int W = NCH * 8;
     const int pf = g.f, pf1 = g.f + 1;
@@ -204,6 +224,13 @@ __device__ void produce(const GatherArgs &g, const Pipe &pp, int pw, int nprod, 
         }
     };
     load_pairs(cur, idx, rv);
+    // lanes with a plain (non-rating) chunk: 16-lane halves own rows 2t and 2t+1
+    const bool c_live = c < NCH && c != pc0 && c != pc1;
+    // swizzled destination of (row 2t + hrow, chunk c) minus its K-block part,
+    // which depends only on t & 3 (operand_addr with k = 2t + hrow)
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int t4 = 0; t4 < 4; ++t4) dst_off[t4] = operand_addr(0, 2 * t4 + hrow, c);
     while (cur.valid()) {
         StageIter nxt = cur;
         for (int k = 0; k < nprod && nxt.valid(); ++k) nxt.next();
@@ -211,7 +238,7 @@ __device__ void produce(const GatherArgs &g, const Pipe &pp, int pw, int nprod, 
         float rv_n[2];
         load_pairs(nxt, idx_n, rv_n);
         const int64_t q0 = cur.q0, p1 = cur.p1;
-        const int s = it % STAGES;
+        const int s = it % NST;
         // rating chunk(s) of rows lane, lane+32: loads issued before the wait
         uint4 pv[2][2];
 #pragma unroll
@@ -222,20 +249,17 @@ __device__ void produce(const GatherArgs &g, const Pipe &pp, int pw, int nprod, 
             pv[h][1] = (ok && pc1 != pc0) ? __ldg(reinterpret_cast<const uint4 *>(row + 8 * pc1))
                                           : make_uint4(0, 0, 0, 0);
         }
-        mbar_wait(pp.empty(s), ((it / STAGES) & 1) ^ 1);
+        mbar_wait_backoff(pp.empty(s), ((it / NST) & 1) ^ 1);
         const uint32_t stg = pp.stage(s);
-#pragma unroll 4
+        const int nrem = static_cast<int>(min(static_cast<int64_t>(KS), p1 - q0));
+#pragma unroll
         for (int t = 0; t < KS / 2; ++t) {
-            const int k = 2 * t + hrow;  // gathered row within the stage
-            const int h = t >> 4;        // uniform: rows < 32 live in idx[0]
-            const int ix = __shfl_sync(0xffffffffu, h ? idx[1] : idx[0], k & 31);
-            const bool valid = q0 + k < p1;
-            if (c < NCH && c != pc0 && c != pc1) {
-                const __half *src = g.fixed16 + static_cast<int64_t>(ix) * W + 8 * c;
-                cp_async16_zfill(operand_addr(stg, k, c),
-                                 valid ? static_cast<const void *>(src) : static_cast<const void *>(g.fixed16),
-                                 valid ? 16u : 0u);
-            }
+            const int k = 2 * t + hrow;
+            // every lane holds (index) pairs for rows lane and lane + 32: full-warp shuffle
+            const int ix = __shfl_sync(0xffffffffu, t < 16 ? idx[0] : idx[1], k & 31);
+            const bool valid = k < nrem;
+            const __half *src = valid ? g.fixed16 + static_cast<int64_t>(ix) * W + 8 * c : g.fixed16;
+            if (c_live) cp_async16_zfill(stg + dst_off[t & 3] + (t >> 2) * KBLK_BYTES, src, valid ? 16u : 0u);
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -273,7 +297,8 @@ __device__ void produce(const GatherArgs &g, const Pipe &pp, int pw, int nprod, 
 
 // Single-thread MMA issuer: one accumulator chain per non-empty row into TMEM
 // buffer (row counter & 1); releases stages with tcgen05.commit.
-__device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe &pp, uint32_t tmem_base, int N,
+template <int NST>
+__device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST> &pp, uint32_t tmem_base, int N,
                                           int64_t row0, int64_t rstride) {
     const uint32_t idesc = make_idesc(M, N);
     uint32_t it = 0, rowc = 0;
@@ -286,8 +311,8 @@ __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe &pp, u
         const uint32_t tmem_d = tmem_base + b * 128;
         uint32_t acc = 0;
         for (int64_t q0 = p0; q0 < p1; q0 += KS, ++it) {
-            const int s = it % STAGES;
-            mbar_wait(pp.full(s), (it / STAGES) & 1);
+            const int s = it % NST;
+            mbar_wait(pp.full(s), (it / NST) & 1);
             tc_fence_after();
             const int nb = static_cast<int>(min(static_cast<int64_t>(KS), p1 - q0));
             const uint32_t sbase = pp.stage(s);

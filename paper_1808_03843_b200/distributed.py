@@ -83,7 +83,7 @@ class ShardedALS:
         self.f, self.lam, self.solver = f, lam, solver
         self.weighted_reg = weighted_reg
         self.rank, self.world, self.group = rank, world, group
-        self.gram_kernel = resolve_gram_kernel(gram_kernel, solver)
+        self.gram_kernel = resolve_gram_kernel(gram_kernel, solver, f)
         dev = ratings.row_ptr.device
         self.m, self.n = ratings.m, ratings.n
         self.xb = shard_bounds(ratings.row_ptr, world)

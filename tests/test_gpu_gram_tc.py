@@ -100,3 +100,25 @@ def test_tc_train_rmse_trajectory_ml1m(golden, cuda_device):
         _, _, rep = cmfb.train(sr, te, cfg)
         traj = np.array(rep.rmse_trajectory())
         assert np.abs(traj - g[solver + "_rmse"]).max() < 1e-3, (solver, traj)
+
+
+def test_fused_tc_cg_matches_two_step(cuda_device):
+    """update_side with the fused kernel (Gram in TMEM -> CG in registers) vs the
+    two-step tensor-core path (packed fp32 A_u in HBM -> batched CG kernel):
+    same fp16 Gram operands, same CG recurrence, so the solutions agree to fp32
+    rounding; rows without ratings are untouched in both."""
+    import torch
+    for f, (m, n, nnz) in ((100, (300, 900, 30000)), (32, (500, 200, 8000)), (8, (50, 40, 300))):
+        t, _ = cmfb.gen_synthetic(m, n, f, nnz / (m * n), 0.1, 3)
+        sr = cmfb.build(t, m + 1, n)  # last user has no ratings
+        theta = cmfb.init_factors(n, f, 0.1, [0, 1])
+        outs = []
+        for kern in ("tc", "tc_unfused"):
+            x = cmfb.init_factors(m + 1, f, 0.1, [0, 0])
+            cmfb.update_side(sr.csr_view(), theta, x, 0.05,
+                             cmfb.SolverConfig("cg", precision="fp32"), gram_kernel=kern)
+            outs.append(x)
+        x0 = cmfb.init_factors(m + 1, f, 0.1, [0, 0])
+        assert np.array_equal(outs[0][m], x0[m]) and np.array_equal(outs[1][m], x0[m])
+        rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1])
+        assert rel < 1e-4, (f, rel)
