@@ -45,8 +45,8 @@ for sname in args.solvers.split(","):
             else:
                 view, fixed, target = train.csc_view(), x, th
             plan = HalfUpdatePlan(view.nrows, f, solver, x.device)
-            tg = target.clone()
             for rep in range(args.reps + 1):
+                tg = target.clone()  # fresh warm start each rep (a solved target exits CG early)
                 rec = {}
                 plan.launch(view.indptr, view.indices, view.values, fixed, tg, 0.05, True, kern, rec)
                 torch.cuda.synchronize()
