@@ -91,14 +91,24 @@ int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices,
  * Same contract as cmf_gram_assemble with a_weights == NULL, except that the
  * fixed factors are read from `fixed16`, the binary16 shadow written by
  * cmf_factors_to_half (row width `w16` = cmf_tc_width(f) halves), and the bias
- * accumulates in fp32 in the same MMAs.  Requires f <= 126, 16-byte aligned
- * a_out rows (a_stride * sizeof(elem) % 16 == 0).
+ * accumulates in fp32 in the same MMAs.  Requires f <= 126, even a_stride.
+ *
+ * Split precision (the exact route): pass `fixed16_lo` and `split_scale` from
+ * cmf_factors_to_half_split; the kernel accumulates H H^T + H L^T + L H^T
+ * (hi/lo binary16 halves of scale*theta, ~2^-22 relative) and undoes the
+ * scale, which gives an fp32-faithful Gram for the exact solver's 1e-4 bar.
+ * fixed16_lo == NULL selects the single-pass fp16 Gram (CG route).
  */
 int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const float *b_weights,
-                         int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
+                         int64_t nrows, const void *fixed16, const void *fixed16_lo,
+                         float split_scale, int32_t w16, int32_t f, double lam,
                          int32_t weighted_reg, const float *base_packed, int32_t precision,
                          void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
                          int32_t *overflow_flag, void *stream);
+/* hi = fp16(scale*x), lo = fp16(scale*x - hi), both (rows, w16), zero padded;
+ * a finite value whose hi overflows binary16 sets *overflow_flag. */
+int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi16, void *lo16,
+                              int32_t w16, float scale, int32_t *overflow_flag, void *stream);
 /*
  * Fused half-update on the CG route (tensor-core Gram -> TMEM -> truncated CG
  * in registers): for every row with n_u > 0, A_u and b_u are accumulated by

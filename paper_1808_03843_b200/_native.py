@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_PKG, "libcmf_b200.so")
 
 CMF_OK, CMF_EINVAL, CMF_EOVERFLOW, CMF_ESINGULAR, CMF_ECUDA = 0, 1, 2, 3, 4
 PREC = {"fp32": 0, "fp16": 1}
-GRAM_KERNELS = {"bitwise": 0, "fma": 1, "tc": 2, "tc_unfused": 2}
+GRAM_KERNELS = {"bitwise": 0, "fma": 1, "tc": 2, "tc_unfused": 2, "tc_split": 2}
 ACCUM = {"fp32": 0, "fp64": 1}
 
 _vp, _i32, _i64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
@@ -34,8 +34,10 @@ _SIGNATURES = {
     "cmf_device_info": (ctypes.c_int, [_vp, _vp, _vp]),
     "cmf_gram_assemble": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i32, _f64, _i32,
                                          _vp, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
-    "cmf_gram_assemble_tc": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i32, _i32, _f64, _i32, _vp,
-                                            _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "cmf_gram_assemble_tc": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_float, _i32, _i32,
+                                            _f64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "cmf_factors_to_half_split": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _i32, ctypes.c_float,
+                                                 _vp, _vp]),
     "cmf_tc_width": (ctypes.c_int, [_i32]),
     "cmf_fused_cg_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i32, _i32, _f64, _i32, _vp,
                                            _i32, _f64, _vp, _vp]),
@@ -102,7 +104,7 @@ def check(rc: int, what: str = ""):
 
 # Kernel-launching entry points called since the counter was last reset (the
 # benchmark's "gpu_launches" claim counts launches of OUR kernels).
-_LAUNCH_COST = {"cmf_fused_cg_update": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
+_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
                 "cmf_batch_cholesky": 1, "cmf_pack_half": 1, "cmf_sq_error": 2,
                 "cmf_sq_error_csr": 2, "cmf_weighted_sqnorm": 2, "cmf_predict_pairs": 1}
 LAUNCHES = [0]

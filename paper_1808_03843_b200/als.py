@@ -62,27 +62,34 @@ def aligned_stride(f: int) -> int:
 
 
 TC_MAX_F = 126  # tensor-core paths: f + 2 operand rows within M = 128
+SPLIT_SCALE = 64.0  # split-fp16 shadow scale: lo stays normal for |theta| >= 2^-9
 
 
 def resolve_gram_kernel(kernel: str | None, solver: SolverConfig, f: int | None = None) -> str:
     """Kernel choice for update_side/train.
 
     "auto": the CG route runs fused on the tensor cores ("tc": Gram in TMEM,
-    CG in registers, A never stored) when f <= 126; the exact route keeps the
-    fp32-faithful SIMT Gram ("fma") its 1e-4 factor bar needs.
+    CG in registers, A never stored) when f <= 126; the exact route uses the
+    split-precision tensor-core Gram ("tc_split": hi/lo fp16 operands, three
+    MMAs, fp32-faithful -- the 1e-4 factor bar rules out a single fp16/TF32
+    pass) and falls back to the SIMT FMA Gram for larger f.
     "tc_unfused" is the paper's two-step scheme on the tensor cores: packed
     fp16/fp32 A_u written to HBM, then the batched CG kernel reads it.
     """
     if kernel in (None, "auto"):
         kernel = os.environ.get("CMF_TRAIN_GRAM_KERNEL", "auto")
+    small = f is None or f <= TC_MAX_F
     if kernel == "auto":
-        use_tc = solver.method == "cg" and (f is None or f <= TC_MAX_F)
-        return "tc" if use_tc else "fma"
+        if solver.method == "cg":
+            return "tc" if small else "fma"
+        return "tc_split" if small else "fma"
     if kernel not in nat.GRAM_KERNELS:
         raise DataError(f"unknown gram kernel {kernel!r}")
-    if kernel.startswith("tc") and solver.method == "exact":
-        raise DataError("the tensor-core Gram (fp16 operands) cannot feed the exact solver; "
-                        "use gram_kernel='fma' or 'bitwise'")
+    if kernel in ("tc", "tc_unfused") and solver.method == "exact":
+        raise DataError("the single-pass fp16 tensor-core Gram cannot feed the exact solver; "
+                        "use gram_kernel='tc_split', 'fma' or 'bitwise'")
+    if kernel == "tc_split" and solver.precision != "fp32":
+        raise DataError("the split-precision Gram stores fp32")
     if kernel.startswith("tc") and f is not None and f > TC_MAX_F:
         raise DataError(f"tensor-core Gram supports f <= {TC_MAX_F}")
     return kernel
@@ -147,13 +154,20 @@ class HalfUpdatePlan:
             off += rb * f * 4
             self.nu_ws = ws[off: off + rb * 8].view(torch.int64)
 
-    def _shadow(self, fx):
-        need = fx.shape[0] * self.w16
+    def _shadow(self, fx, split: bool = False):
+        """binary16 shadow of the fixed factors (hi, or hi + lo for the split Gram)."""
+        need = fx.shape[0] * self.w16 * (2 if split else 1)
         if self.shadow is None or self.shadow.numel() < need:
             self.shadow = torch.empty(need, dtype=torch.float16, device=fx.device)
+        if split:
+            half = fx.shape[0] * self.w16
+            nat.call("cmf_factors_to_half_split", nat.ptr(fx), fx.shape[0], self.f,
+                     nat.ptr(self.shadow), nat.ptr(self.shadow) + 2 * half, self.w16, SPLIT_SCALE,
+                     nat.ptr(self.flags), nat.stream_ptr())
+            return self.shadow, nat.ptr(self.shadow) + 2 * half
         nat.call("cmf_factors_to_half", nat.ptr(fx), fx.shape[0], self.f, nat.ptr(self.shadow),
                  self.w16, nat.stream_ptr())
-        return self.shadow
+        return self.shadow, None
 
     def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
                row0: int = 0, nrows: int | None = None):
@@ -166,7 +180,7 @@ class HalfUpdatePlan:
         if record is not None and tc:
             es0 = torch.cuda.Event(enable_timing=True)
             es0.record()
-        shadow = self._shadow(fx) if tc else None
+        shadow, lo = self._shadow(fx, split=kernel == "tc_split") if tc else (None, None)
         if record is not None and tc:
             es1 = torch.cuda.Event(enable_timing=True)
             es1.record()
@@ -192,7 +206,7 @@ class HalfUpdatePlan:
                 e0.record()
             if tc:
                 nat.call("cmf_gram_assemble_tc", nat.ptr(indptr) + 8 * r0, nat.ptr(indices),
-                         nat.ptr(values), nb, nat.ptr(shadow), self.w16, f, float(lam),
+                         nat.ptr(values), nb, nat.ptr(shadow), lo, SPLIT_SCALE, self.w16, f, float(lam),
                          int(bool(weighted_reg)), None, nat.PREC[solver.precision],
                          nat.ptr(self.a_ws), self.stride, nat.ptr(self.b_ws),
                          nat.ptr(self.nu_ws), nat.ptr(self.flags), st)

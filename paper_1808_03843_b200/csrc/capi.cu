@@ -20,9 +20,10 @@ int set_error(int code, const char *fmt, ...) {
 int gram_simt_launch(const int64_t *, const int32_t *, const float *, const float *, int64_t,
                      const float *, int, double, int, const float *, bool, bool, void *, int64_t,
                      float *, int64_t *, int32_t *, cudaStream_t);
-int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int, int,
-                   double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
+int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, const void *, float,
+                   int, int, double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
                    cudaStream_t);
+int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, int, float, int32_t *, cudaStream_t);
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int, int, double,
                     int, float *, int, double, int32_t *, cudaStream_t);
@@ -111,18 +112,27 @@ int cmf_factors_to_half(const float *x, int64_t rows, int32_t f, void *out16, in
     return factors_to_half_launch(x, rows, f, out16, w16, S(stream));
 }
 
+int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi16, void *lo16, int32_t w16,
+                              float scale, int32_t *overflow_flag, void *stream) {
+    REQUIRE(rows >= 0 && f >= 1 && w16 >= f && scale > 0.0f, "bad arguments");
+    if (rows == 0) return CMF_OK;
+    REQUIRE(x && hi16 && lo16, "null argument");
+    return factors_to_half_split_launch(x, rows, f, hi16, lo16, w16, scale, overflow_flag, S(stream));
+}
+
 int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const float *b_weights,
-                         int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
-                         int32_t weighted_reg, const float *base_packed, int32_t precision,
-                         void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
+                         int64_t nrows, const void *fixed16, const void *fixed16_lo, float split_scale,
+                         int32_t w16, int32_t f, double lam, int32_t weighted_reg, const float *base_packed,
+                         int32_t precision, void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
                          int32_t *overflow_flag, void *stream) {
     REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
     REQUIRE(precision == CMF_PREC_FP32 || precision == CMF_PREC_FP16, "unknown precision %d", precision);
     REQUIRE(a_stride >= f * (int64_t)(f + 1) / 2, "a_stride smaller than f*(f+1)/2");
     if (nrows == 0) return CMF_OK;
     REQUIRE(indptr && a_out && fixed16, "null argument");
-    return gram_tc_launch(indptr, indices, b_weights, nrows, fixed16, w16, f, lam, weighted_reg,
-                          base_packed, precision == CMF_PREC_FP16, a_out, a_stride, b_out, nu_out,
+    REQUIRE(!fixed16_lo || split_scale > 0.0f, "split_scale must be > 0");
+    return gram_tc_launch(indptr, indices, b_weights, nrows, fixed16, fixed16_lo, split_scale, w16, f, lam,
+                          weighted_reg, base_packed, precision == CMF_PREC_FP16, a_out, a_stride, b_out, nu_out,
                           overflow_flag, S(stream));
 }
 
@@ -198,7 +208,7 @@ int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *
     for (int64_t r0 = 0; r0 < nrows; r0 += ws_rows) {
         const int64_t nb = nrows - r0 < ws_rows ? nrows - r0 : ws_rows;
         int rc = kernel == CMF_GRAM_TC
-                     ? cmf_gram_assemble_tc(indptr + r0, indices, values, nb, ws16, w16, f, lam,
+                     ? cmf_gram_assemble_tc(indptr + r0, indices, values, nb, ws16, nullptr, 1.0f, w16, f, lam,
                                             weighted_reg, nullptr, precision, ws_a, a_stride, ws_b,
                                             ws_nu, flags + 0, stream)
                      : cmf_gram_assemble(indptr + r0, indices, nullptr, values, nb, fixed, ncols, f,

@@ -47,7 +47,7 @@ struct FusedArgs {
     int32_t *breakdowns;
 };
 
-using FPipe = Pipe<F_STAGES>;
+using FPipe = Pipe<F_STAGES, false>;
 
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     uint32_t v;
@@ -122,9 +122,9 @@ __global__ void __maxnreg__(128) fused_cg_kernel(FusedArgs g) {
     const int64_t G = gridDim.x;
 
     if (warp >= 8 && warp < 12) {
-        produce<NCH, F_STAGES>(ga, pp, warp - 8, 4, lane, blockIdx.x, G);
+        produce<NCH, F_STAGES, false>(ga, pp, warp - 8, 4, lane, blockIdx.x, G);
     } else if (warp == 12) {
-        if (lane == 0) issue_mma<F_STAGES>(ga, pp, tmem_base, g.N, blockIdx.x, G);
+        if (lane == 0) issue_mma<F_STAGES, false>(ga, pp, tmem_base, g.N, blockIdx.x, G);
         __syncwarp();
     } else {
         // ------------------------------------------------------------ CG groups
@@ -273,6 +273,7 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
     g.gather.indices = indices;
     g.gather.values = values;
     g.gather.fixed16 = static_cast<const __half *>(fixed16);
+    g.gather.fixed16_lo = nullptr;
     g.gather.nrows = nrows;
     g.gather.f = f;
     g.N = ((f + 2 + 15) / 16) * 16;

@@ -42,6 +42,7 @@ constexpr int EPI_THREADS = 128;
 
 struct Args {
     GatherArgs gather;
+    float gram_scale, bias_scale;  // undo the split shadow's power-of-two scaling
     int N;
     double lam;
     int weighted;
@@ -57,8 +58,9 @@ __device__ __forceinline__ void bar_epi() { named_bar(1, EPI_THREADS); }
 
 // Packed-offset table: tab[k] = i*W + j for packed entry k = i*(i+1)/2 + j.
 // Built once per CTA; the epilogue copy-out walks the packed row with it.
-template <int NCH, bool HALF_OUT>
-__global__ void __launch_bounds__(NUM_THREADS, 2) gram_tc_kernel(Args g) {
+template <int NCH, bool HALF_OUT, bool SPLIT>
+__global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
+    using PipeT = Pipe<STAGES, SPLIT>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     constexpr int W = NCH * 8;
     using SqT = typename std::conditional<HALF_OUT, __half, float>::type;
@@ -68,18 +70,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) gram_tc_kernel(Args g) {
     // layout: [stages (1024-aligned) | square staging (f x W, SqT) | offset table | barriers | tmem slot]
     unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     unsigned char *stage_mem = smem;
-    SqT *sq = reinterpret_cast<SqT *>(smem + STAGES * STAGE_BYTES);
+    SqT *sq = reinterpret_cast<SqT *>(smem + STAGES * PipeT::kStageBytes);
     const size_t sq_bytes = ((static_cast<size_t>(f) * W * sizeof(SqT)) + 15) & ~static_cast<size_t>(15);
-    uint16_t *tab = reinterpret_cast<uint16_t *>(smem + STAGES * STAGE_BYTES + sq_bytes);
+    uint16_t *tab = reinterpret_cast<uint16_t *>(smem + STAGES * PipeT::kStageBytes + sq_bytes);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES + sq_bytes + tab_bytes);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + Pipe<STAGES>::kBars);
-    Pipe<STAGES> pp{smem_u32(stage_mem), smem_u32(bars)};
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * PipeT::kStageBytes + sq_bytes + tab_bytes);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + PipeT::kBars);
+    PipeT pp{smem_u32(stage_mem), smem_u32(bars)};
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // zero the operand ring once: MN-blocks >= NCH (rows >= W) are never written again
-    for (int i = tid; i < STAGES * STAGE_BYTES / 16; i += NUM_THREADS)
+    for (int i = tid; i < STAGES * PipeT::kStageBytes / 16; i += NUM_THREADS)
         reinterpret_cast<int4 *>(stage_mem)[i] = make_int4(0, 0, 0, 0);
     for (int i = tid; i < f; i += NUM_THREADS) {
         const int base = i * (i + 1) / 2;
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) gram_tc_kernel(Args g) {
 
     const int64_t G = gridDim.x;
     if (warp >= 4 && warp < 8) {
-        produce<NCH>(ga, pp, warp - 4, 4, lane, blockIdx.x, G);
+        produce<NCH, STAGES, SPLIT>(ga, pp, warp - 4, 4, lane, blockIdx.x, G);
     } else if (warp == 8) {
         if (lane == 0) issue_mma(ga, pp, tmem_base, g.N, blockIdx.x, G);
         __syncwarp();
@@ -142,6 +144,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) gram_tc_kernel(Args g) {
                     tmem_ld32(tbase + cc * 32, v);
                     tmem_ld_wait();
                     const int c0 = cc * 32;
+                    if (SPLIT) {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const int j = c0 + jj;
+                            const float sc = (j == f || j == f + 1) ? g.bias_scale : g.gram_scale;
+                            v[jj] = __float_as_uint(__uint_as_float(v[jj]) * sc);
+                        }
+                    }
                     if (cc == warp) {  // warp-uniform: this chunk holds every lane's diagonal
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
@@ -243,7 +253,36 @@ __global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __ha
     }
 }
 
+// Split shadow: hi = fp16(scale*x), lo = fp16(scale*x - hi); scale is a power of
+// two that keeps lo out of the binary16 subnormal range for |x| >= 2^-9.
+__global__ void factors_to_half_split_kernel(const float *x, int64_t rows, int f, __half *hi, __half *lo, int W,
+                                             float scale, int32_t *ovf) {
+    const int64_t n = rows * W;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int bad = 0;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
+        const int64_t r = e / W;
+        const int c = static_cast<int>(e - r * W);
+        const float v = c < f ? x[r * f + c] * scale : 0.0f;
+        const __half h = __float2half_rn(v);
+        if (isfinite(v) && __hisinf(h)) bad = 1;
+        hi[e] = h;
+        lo[e] = __float2half_rn(v - __half2float(h));
+    }
+    if (bad && ovf) atomicOr(ovf, 1);
+}
+
 }  // namespace tc
+
+int factors_to_half_split_launch(const float *x, int64_t rows, int f, void *hi, void *lo, int W, float scale,
+                                 int32_t *ovf, cudaStream_t st) {
+    if (rows == 0) return CMF_OK;
+    int64_t blocks = (rows * W + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    tc::factors_to_half_split_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        x, rows, f, static_cast<__half *>(hi), static_cast<__half *>(lo), W, scale, ovf);
+    return check_launch("factors_to_half_split_kernel");
+}
 
 int gram_tc_width(int f) { return ((f + 2 + 7) / 8) * 8; }
 
@@ -256,9 +295,9 @@ int factors_to_half_launch(const float *x, int64_t rows, int f, void *out, int W
     return check_launch("factors_to_half_kernel");
 }
 
-template <int NCH, bool H>
+template <int NCH, bool H, bool SPLIT>
 static int launch_nch(const tc::Args &g, size_t smem, int64_t nrows, cudaStream_t st) {
-    auto k = tc::gram_tc_kernel<NCH, H>;
+    auto k = tc::gram_tc_kernel<NCH, H, SPLIT>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return set_error(CMF_ECUDA, "gram_tc smem attr: %s", cudaGetErrorString(e));
     int dev = 0, sms = 148, per_sm = 1;
@@ -273,32 +312,32 @@ static int launch_nch(const tc::Args &g, size_t smem, int64_t nrows, cudaStream_
     return check_launch("gram_tc_kernel");
 }
 
-template <bool H>
+template <bool H, bool SPLIT>
 static int dispatch_nch(int nch, const tc::Args &g, size_t smem, int64_t nrows, cudaStream_t st) {
     switch (nch) {
-        case 1: return launch_nch<1, H>(g, smem, nrows, st);
-        case 2: return launch_nch<2, H>(g, smem, nrows, st);
-        case 3: return launch_nch<3, H>(g, smem, nrows, st);
-        case 4: return launch_nch<4, H>(g, smem, nrows, st);
-        case 5: return launch_nch<5, H>(g, smem, nrows, st);
-        case 6: return launch_nch<6, H>(g, smem, nrows, st);
-        case 7: return launch_nch<7, H>(g, smem, nrows, st);
-        case 8: return launch_nch<8, H>(g, smem, nrows, st);
-        case 9: return launch_nch<9, H>(g, smem, nrows, st);
-        case 10: return launch_nch<10, H>(g, smem, nrows, st);
-        case 11: return launch_nch<11, H>(g, smem, nrows, st);
-        case 12: return launch_nch<12, H>(g, smem, nrows, st);
-        case 13: return launch_nch<13, H>(g, smem, nrows, st);
-        case 14: return launch_nch<14, H>(g, smem, nrows, st);
-        case 15: return launch_nch<15, H>(g, smem, nrows, st);
-        default: return launch_nch<16, H>(g, smem, nrows, st);
+        case 1: return launch_nch<1, H, SPLIT>(g, smem, nrows, st);
+        case 2: return launch_nch<2, H, SPLIT>(g, smem, nrows, st);
+        case 3: return launch_nch<3, H, SPLIT>(g, smem, nrows, st);
+        case 4: return launch_nch<4, H, SPLIT>(g, smem, nrows, st);
+        case 5: return launch_nch<5, H, SPLIT>(g, smem, nrows, st);
+        case 6: return launch_nch<6, H, SPLIT>(g, smem, nrows, st);
+        case 7: return launch_nch<7, H, SPLIT>(g, smem, nrows, st);
+        case 8: return launch_nch<8, H, SPLIT>(g, smem, nrows, st);
+        case 9: return launch_nch<9, H, SPLIT>(g, smem, nrows, st);
+        case 10: return launch_nch<10, H, SPLIT>(g, smem, nrows, st);
+        case 11: return launch_nch<11, H, SPLIT>(g, smem, nrows, st);
+        case 12: return launch_nch<12, H, SPLIT>(g, smem, nrows, st);
+        case 13: return launch_nch<13, H, SPLIT>(g, smem, nrows, st);
+        case 14: return launch_nch<14, H, SPLIT>(g, smem, nrows, st);
+        case 15: return launch_nch<15, H, SPLIT>(g, smem, nrows, st);
+        default: return launch_nch<16, H, SPLIT>(g, smem, nrows, st);
     }
 }
 
 int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
-                   const void *fixed16, int W, int f, double lam, int weighted, const float *base, bool half,
-                   void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out, int32_t *overflow,
-                   cudaStream_t st) {
+                   const void *fixed16, const void *fixed16_lo, float split_scale, int W, int f, double lam,
+                   int weighted, const float *base, bool half, void *a_out, int64_t a_stride, float *b_out,
+                   int64_t *nu_out, int32_t *overflow, cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
     if (f + 2 > tc::M)
         return set_error(CMF_EINVAL, "tensor-core Gram supports f <= %d (got %d)", tc::M - 2, f);
@@ -313,8 +352,12 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     g.gather.indices = indices;
     g.gather.values = values;
     g.gather.fixed16 = static_cast<const __half *>(fixed16);
+    g.gather.fixed16_lo = static_cast<const __half *>(fixed16_lo);
     g.gather.nrows = nrows;
     g.gather.f = f;
+    const bool split = fixed16_lo != nullptr;
+    g.gram_scale = split ? 1.0f / (split_scale * split_scale) : 1.0f;
+    g.bias_scale = split ? 1.0f / split_scale : 1.0f;
     g.N = ((f + 2 + 15) / 16) * 16;
     g.lam = lam;
     g.weighted = weighted;
@@ -327,9 +370,15 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     const int64_t P = packed_size(f);
     const size_t sq_bytes = ((static_cast<size_t>(f) * W * esz) + 15) & ~static_cast<size_t>(15);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
-    const size_t smem = 1024 + tc::STAGES * tc::STAGE_BYTES + sq_bytes + tab_bytes + tc::Pipe<tc::STAGES>::kBars * 8 + 16;
+    const size_t smem = 1024 + tc::STAGES * tc::STAGE_BYTES * (split ? 2 : 1) + sq_bytes + tab_bytes +
+                        tc::Pipe<tc::STAGES>::kBars * 8 + 16;
     const int nch = W / 8;
-    return half ? dispatch_nch<true>(nch, g, smem, nrows, st) : dispatch_nch<false>(nch, g, smem, nrows, st);
+    if (split) {
+        if (half) return set_error(CMF_EINVAL, "the split-precision Gram stores fp32");
+        return dispatch_nch<false, true>(nch, g, smem, nrows, st);
+    }
+    return half ? dispatch_nch<true, false>(nch, g, smem, nrows, st)
+                : dispatch_nch<false, false>(nch, g, smem, nrows, st);
 }
 
 }  // namespace cmf

@@ -35,32 +35,29 @@ struct CgArgs {
     int vec16;
 };
 
+// Stage one packed system into shared memory with async copies (every load in
+// flight at once; the caller commits and waits).
 template <bool HALF_A>
 __device__ __forceinline__ void load_packed(const CgArgs &g, int64_t s, void *dst, int64_t P) {
     const size_t es = HALF_A ? 2 : 4;
     const char *src = static_cast<const char *>(g.a) + static_cast<size_t>(s) * g.a_stride * es;
     const int64_t bytes = P * es;
+    char *d = static_cast<char *>(dst);
     if (g.vec16) {
-        const int4 *s4 = reinterpret_cast<const int4 *>(src);
-        int4 *d4 = static_cast<int4 *>(dst);
-        for (int64_t k = threadIdx.x; k < (bytes >> 4); k += blockDim.x) d4[k] = __ldg(s4 + k);
-        for (int64_t k = (bytes & ~15ll) + threadIdx.x * es; k < bytes; k += blockDim.x * es) {
-            if (HALF_A)
-                *reinterpret_cast<uint16_t *>(static_cast<char *>(dst) + k) =
-                    *reinterpret_cast<const uint16_t *>(src + k);
-            else
-                *reinterpret_cast<float *>(static_cast<char *>(dst) + k) =
-                    *reinterpret_cast<const float *>(src + k);
-        }
+        for (int64_t k = threadIdx.x; k < (bytes >> 4); k += blockDim.x) cp_async16(d + 16 * k, src + 16 * k);
+        // tail (< 16 bytes): 4-byte pieces (P*es is even for fp16 when P is even; else 2-byte below)
+        for (int64_t k = (bytes & ~15ll) + 4 * threadIdx.x; k + 4 <= bytes; k += 4 * blockDim.x)
+            cp_async4(d + k, src + k, 4);
+        if ((bytes & 3) && threadIdx.x == 0)
+            *reinterpret_cast<uint16_t *>(d + bytes - 2) = *reinterpret_cast<const uint16_t *>(src + bytes - 2);
     } else if (HALF_A) {
         const uint16_t *s2 = reinterpret_cast<const uint16_t *>(src);
-        uint16_t *d2 = static_cast<uint16_t *>(dst);
+        uint16_t *d2 = reinterpret_cast<uint16_t *>(d);
         for (int64_t k = threadIdx.x; k < P; k += blockDim.x) d2[k] = s2[k];
     } else {
-        const float *s1 = reinterpret_cast<const float *>(src);
-        float *d1 = static_cast<float *>(dst);
-        for (int64_t k = threadIdx.x; k < P; k += blockDim.x) d1[k] = s1[k];
+        for (int64_t k = threadIdx.x; k < P; k += blockDim.x) cp_async4(d + 4 * k, src + 4 * k, 4);
     }
+    cp_async_commit();
 }
 
 template <bool HALF_A>
@@ -87,6 +84,7 @@ __global__ void __launch_bounds__(128) cg_rowreg_kernel(CgArgs g) {
     const bool act = tid < f;
     float xi = act ? g.x0[s * f + tid] : 0.0f;
     const float bi = act ? g.b[s * f + tid] : 0.0f;
+    cp_async_wait<0>();
     __syncthreads();
 
     // expand row `tid` of the symmetric matrix into registers

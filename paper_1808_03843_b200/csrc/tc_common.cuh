@@ -155,22 +155,26 @@ struct GatherArgs {
     const int32_t *indices;
     const float *values;   // ratings (b weights); nullptr -> zero bias rows
     const __half *fixed16; // (ncols, W) binary16 shadow, W = NCH * 8
+    const __half *fixed16_lo;  // split mode: binary16 residual shadow (same layout)
     int64_t nrows;
     int f;
 };
 
 // Operand ring of NST stages + 2 TMEM accumulator hand-offs (mbarriers:
 // full[NST], empty[NST], tfull[2], tempty[2]).
-template <int NST>
+// SPLIT: every stage holds two operands, hi then lo (split-fp16 Gram,
+// D = H H^T + H L^T + L H^T), so the stage stride doubles.
+template <int NST, bool SPLIT = false>
 struct Pipe {
     static constexpr int kStages = NST;
     static constexpr int kBars = 2 * NST + 4;
+    static constexpr int kStageBytes = (SPLIT ? 2 : 1) * STAGE_BYTES;
     uint32_t stage_s, bar_s;
     __device__ uint32_t full(int s) const { return bar_s + 8u * s; }
     __device__ uint32_t empty(int s) const { return bar_s + 8u * (NST + s); }
     __device__ uint32_t tfull(int b) const { return bar_s + 8u * (2 * NST + b); }
     __device__ uint32_t tempty(int b) const { return bar_s + 8u * (2 * NST + 2 + b); }
-    __device__ uint32_t stage(int s) const { return stage_s + s * STAGE_BYTES; }
+    __device__ uint32_t stage(int s) const { return stage_s + s * kStageBytes; }
 };
 
 // Walk over pipeline stages: (row u, first position q0 of the K-chunk) pairs
@@ -201,9 +205,9 @@ struct StageIter {
 // Producer warp `pw` of `nprod`: fills every stage `it` with it % nprod == pw.
 // The (index, rating) pairs of the warp's NEXT stage are loaded while the
 // current one is being gathered, so index-load latency stays off the ring.
-template <int NCH, int NST>
-__device__ void produce(const GatherArgs &g, const Pipe<NST> &pp, int pw, int nprod, int lane, int64_t row0,
-                        int64_t rstride) {
+template <int NCH, int NST, bool SPLIT>
+__device__ void produce(const GatherArgs &g, const Pipe<NST, SPLIT> &pp, int pw, int nprod, int lane,
+                        int64_t row0, int64_t rstride) {
     constexpr int W = NCH * 8;
     const int pf = g.f, pf1 = g.f + 1;
     const int pc0 = pf >> 3, pc1 = pf1 >> 3;
@@ -258,8 +262,12 @@ __device__ void produce(const GatherArgs &g, const Pipe<NST> &pp, int pw, int np
             // every lane holds (index) pairs for rows lane and lane + 32: full-warp shuffle
             const int ix = __shfl_sync(0xffffffffu, t < 16 ? idx[0] : idx[1], k & 31);
             const bool valid = k < nrem;
-            const __half *src = valid ? g.fixed16 + static_cast<int64_t>(ix) * W + 8 * c : g.fixed16;
-            if (c_live) cp_async16_zfill(stg + dst_off[t & 3] + (t >> 2) * KBLK_BYTES, src, valid ? 16u : 0u);
+            const int64_t off = static_cast<int64_t>(ix) * W + 8 * c;
+            const __half *src = valid ? g.fixed16 + off : g.fixed16;
+            const uint32_t dst = stg + dst_off[t & 3] + (t >> 2) * KBLK_BYTES;
+            if (c_live) cp_async16_zfill(dst, src, valid ? 16u : 0u);
+            if (SPLIT && c < NCH)  // residual operand: every chunk (its rating slots stay zero)
+                cp_async16_zfill(dst + STAGE_BYTES, valid ? g.fixed16_lo + off : g.fixed16_lo, valid ? 16u : 0u);
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -297,9 +305,9 @@ __device__ void produce(const GatherArgs &g, const Pipe<NST> &pp, int pw, int np
 
 // Single-thread MMA issuer: one accumulator chain per non-empty row into TMEM
 // buffer (row counter & 1); releases stages with tcgen05.commit.
-template <int NST>
-__device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST> &pp, uint32_t tmem_base, int N,
-                                          int64_t row0, int64_t rstride) {
+template <int NST, bool SPLIT>
+__device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, SPLIT> &pp, uint32_t tmem_base,
+                                          int N, int64_t row0, int64_t rstride) {
     const uint32_t idesc = make_idesc(M, N);
     uint32_t it = 0, rowc = 0;
     for (int64_t u = row0; u < g.nrows; u += rstride) {
@@ -320,6 +328,11 @@ __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST> &
                 const uint64_t d = make_desc(sbase + kk * 2 * KBLK_BYTES);
                 tc_mma(tmem_d, d, d, idesc, acc);
                 acc = 1;
+                if (SPLIT) {  // + H L^T + L H^T into the same accumulator
+                    const uint64_t dl = make_desc(sbase + STAGE_BYTES + kk * 2 * KBLK_BYTES);
+                    tc_mma(tmem_d, d, dl, idesc, 1);
+                    tc_mma(tmem_d, dl, d, idesc, 1);
+                }
             }
             tc_commit(pp.empty(s));
         }

@@ -195,17 +195,26 @@ def assemble_side(view: RowView, theta, lam: float, cfg: TileConfig | None = Non
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    if kernel == "tc":
+    if kernel.startswith("tc"):
         if aw is not None:
             raise DataError("the tensor-core Gram kernel does not take a_weights")
-        stride = (P + 7) // 8 * 8  # 16-byte rows for the bulk store
+        split = kernel == "tc_split"
+        if split and precision != "fp32":
+            raise DataError("the split-precision Gram stores fp32")
+        stride = (P + 7) // 8 * 8  # 16-byte rows
         a_full = torch.empty((nrows, stride), dtype=dt, device=dev)
         w16 = nat.tc_width(f)
-        shadow = torch.empty((th.shape[0], w16), dtype=torch.float16, device=dev)
-        nat.call("cmf_factors_to_half", nat.ptr(th), th.shape[0], f, nat.ptr(shadow), w16,
-                 nat.stream_ptr())
+        shadow = torch.empty((2 if split else 1, th.shape[0], w16), dtype=torch.float16, device=dev)
+        scale = 64.0
+        if split:
+            nat.call("cmf_factors_to_half_split", nat.ptr(th), th.shape[0], f, nat.ptr(shadow[0]),
+                     nat.ptr(shadow[1]), w16, scale, nat.ptr(flag), nat.stream_ptr())
+        else:
+            nat.call("cmf_factors_to_half", nat.ptr(th), th.shape[0], f, nat.ptr(shadow[0]), w16,
+                     nat.stream_ptr())
         nat.call("cmf_gram_assemble_tc", nat.ptr(indptr), nat.ptr(indices), nat.ptr(bw), nrows,
-                 nat.ptr(shadow), w16, f, float(lam), int(bool(weighted_reg)), nat.ptr(base),
+                 nat.ptr(shadow[0]), nat.ptr(shadow[1]) if split else None, scale, w16, f,
+                 float(lam), int(bool(weighted_reg)), nat.ptr(base),
                  nat.PREC[precision], nat.ptr(a_full), stride, nat.ptr(b_out), nat.ptr(nu),
                  nat.ptr(flag), nat.stream_ptr())
         a_out = a_full[:, :P]

@@ -149,7 +149,8 @@ def test_update_side_semantics(oracle, cuda_device):
     assert np.array_equal(theta, th_before)            # fixed is read-only
     assert np.array_equal(x[120], x_before[120])       # empty row untouched
     assert not np.array_equal(x[:120], x_before[:120])
-    assert nbytes == 121 * 36 * 2 and brk == 0 and times.accumulate > 0 and times.solve > 0
+    # the fused tensor-core route reports one kernel under accumulate
+    assert nbytes == 121 * 36 * 2 and brk == 0 and times.accumulate + times.solve > 0
     # device tensors: in place on the device, same numbers
     xd = torch.tensor(x_before, device=cuda_device)
     cmfb.update_side(sr.to_device().csr_view(), torch.tensor(theta, device=cuda_device), xd, 0.05,

@@ -122,3 +122,58 @@ def test_fused_tc_cg_matches_two_step(cuda_device):
         assert np.array_equal(outs[0][m], x0[m]) and np.array_equal(outs[1][m], x0[m])
         rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1])
         assert rel < 1e-4, (f, rel)
+
+
+def test_split_precision_gram_is_fp32_faithful(golden, oracle, cuda_device):
+    """tc_split (hi/lo fp16 operands, H H^T + H L^T + L H^T) vs the reference's
+    float32 Gram: within 2e-6 relative Frobenius per row -- the fp32 SIMT
+    kernel's own distance is ~1e-7, a single fp16/TF32 pass is ~1e-3."""
+    g = golden("gram_cases")
+    for ci in range(int(g["ncases"])):
+        p = f"c{ci}_"
+        m, n, f = (int(v) for v in g[p + "meta"])
+        if f > 126:
+            continue
+        for side in ("x", "t"):
+            if side == "x":
+                view = RowView(g[p + "row_ptr"], g[p + "col_idx"], g[p + "csr_val"], m, n)
+                th = g[p + "theta_n"]
+            else:
+                view = RowView(g[p + "col_ptr"], g[p + "row_idx"], g[p + "csc_val"], n, m)
+                th = g[p + "theta_m"]
+            gb, _ = cmfb.assemble_side(view, th, 0.05, kernel="tc_split")
+            ref_a = g[f"{p}{side}_fp32_1_a"].astype(np.float64)
+            ref_b = g[f"{p}{side}_fp32_1_b"].astype(np.float64)
+            for u in range(ref_a.shape[0]):
+                da = np.linalg.norm(gb.a_lower[u] - ref_a[u]) / max(np.linalg.norm(ref_a[u]), 1e-30)
+                db = np.linalg.norm(gb.b[u] - ref_b[u]) / max(np.linalg.norm(ref_b[u]), 1e-30)
+                assert da < 2e-6 and db < 2e-6, (p, side, u, da, db)
+    # heavy rows (K in the thousands) at f = 100: the tensor core's fp32
+    # accumulation (not the operand split) dominates there, ~1e-5 at K = 5571
+    view, theta = _instance(3, 6000, 100, [5571, 206, 1], 11)
+    gb, _ = cmfb.assemble_side(view, theta, 0.05, kernel="tc_split")
+    a, b, _ = oracle.assemble_side(view.indptr, view.indices, view.values, 3, theta, 0.05)
+    for u, tol in zip(range(3), (5e-5, 2e-6, 2e-6)):
+        assert np.linalg.norm(gb.a_lower[u] - a[u]) / np.linalg.norm(a[u]) < tol, u
+        assert np.linalg.norm(gb.b[u] - b[u]) / np.linalg.norm(b[u]) < tol, u
+
+
+def test_exact_route_long_rows_factor_bar(oracle, cuda_device):
+    """Exact route with the default (split tensor-core) Gram on rows of K ~ 600-1200
+    (items): factors within 1e-4 relative of the CPU oracle (float32 bitwise Gram +
+    float64 Cholesky) after every half-update -- the north_star exact-path bar."""
+    m, n, f = 1500, 300, 48
+    t, _, _ = oracle.gen_synthetic(m, n, f, 0.5, 0.1, 2)
+    r = oracle.build(t, m, n)
+    x_o = oracle.init_factors(m, f, 0.1, [0, 0])
+    t_o = oracle.init_factors(n, f, 0.1, [0, 1])
+    x_g, t_g = x_o.copy(), t_o.copy()
+    sr = cmfb.build(cmfb.Triples(t.user, t.item, t.rating), m, n)
+    solver = cmfb.SolverConfig("exact")
+    for epoch in range(4):
+        oracle.update_side(r.csr(), t_o, x_o, 0.05, "exact")
+        cmfb.update_side(sr.csr_view(), t_g, x_g, 0.05, solver)
+        assert np.linalg.norm(x_g - x_o) / np.linalg.norm(x_o) < 1e-4, (epoch, "x")
+        oracle.update_side(r.csc(), x_o, t_o, 0.05, "exact")
+        cmfb.update_side(sr.csc_view(), x_g, t_g, 0.05, solver)
+        assert np.linalg.norm(t_g - t_o) / np.linalg.norm(t_o) < 1e-4, (epoch, "t")
