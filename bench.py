@@ -300,8 +300,7 @@ def main():
     per_kernel = {}
     for name, lst in resolve_events(kern).items():
         per_kernel[name] = {"ms_total": sum(lst), "launches": len(lst)}
-    gram_ms = sum(v["ms_total"] for k, v in per_kernel.items()
-                  if k.startswith("gram") or k == "shadow16")
+    gram_ms = sum(v["ms_total"] for k, v in per_kernel.items() if k.startswith("gram"))
     solve_ms = sum(v["ms_total"] for k, v in per_kernel.items() if k.startswith("solve"))
     fused_ms = sum(v["ms_total"] for k, v in per_kernel.items() if k.startswith("fused"))
     gram_flops_step = 2.0 * P * (shard_nnz["x"] + shard_nnz["t"])
@@ -371,7 +370,7 @@ def main():
     if not args.no_exact and method != "exact":
         ex_engine = cdist.ShardedALS(train, f, lam=0.05,
                                      solver=cmfb.SolverConfig("exact"),
-                                     gram_kernel="fma", rank=rank, world=world)
+                                     gram_kernel="auto", rank=rank, world=world)
         xe, the = x0.clone(), th0.clone()
         for _ in range(2):
             ex_engine.iteration(xe, the)
@@ -390,7 +389,10 @@ def main():
         result["exact"] = {"workload": f"{args.shape}-f{f}-exact (BASELINE configs[1])",
                            "sec_per_iteration": ems / 1e3,
                            "gram_ms": sum(sum(v) for k, v in kx.items() if k.startswith("gram")) / max(2, args.steps // 2),
-                           "solve_ms": sum(sum(v) for k, v in kx.items() if k.startswith("solve")) / max(2, args.steps // 2)}
+                           "solve_ms": sum(sum(v) for k, v in kx.items() if k.startswith("solve")) / max(2, args.steps // 2),
+                           "gram_kernel": ex_engine.gram_kernel,
+                           "per_kernel_ms_per_step": {k: sum(v) / max(2, args.steps // 2)
+                                                      for k, v in kx.items()}}
         del ex_engine
 
     # ---- time to RMSE (fresh start; per-epoch eval excluded from the clock)

@@ -23,7 +23,7 @@
 
 namespace cmf {
 
-__device__ __forceinline__ int tri_row_t(int t) {
+__device__ __forceinline__ int tri_row_unused(int t) {
     int r = static_cast<int>((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
     while ((r + 1) * (r + 2) / 2 <= t) ++r;
     while (r * (r + 1) / 2 > t) --r;
@@ -31,7 +31,7 @@ __device__ __forceinline__ int tri_row_t(int t) {
 }
 
 template <int TPT>
-__global__ void __launch_bounds__(128, 4) chol_tiled_kernel(const float *A, int64_t a_stride, const float *B,
+__global__ void __launch_bounds__(128, 7) chol_tiled_kernel(const float *A, int64_t a_stride, const float *B,
                                                          const int64_t *nu, int64_t nsys, int f, float *X,
                                                          int32_t *info, int32_t *nbad) {
     extern __shared__ __align__(16) float csm[];
@@ -66,13 +66,21 @@ __global__ void __launch_bounds__(128, 4) chol_tiled_kernel(const float *A, int6
     int ti[TPT], tj[TPT];
     bool valid[TPT];
     float a[TPT][4][4];
+    // Tiles are numbered column-major (by tj, then ti) and dealt round-robin:
+    // the tiles still active at panel p (tj > p) are then a contiguous suffix
+    // of the numbering, so whole warps drop out as the trailing matrix
+    // shrinks instead of every warp carrying a few active lanes.
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
         const int t = tid + q * NT;
         valid[q] = t < T;
-        const int r = valid[q] ? tri_row_t(t) : 0;
-        ti[q] = r;
-        tj[q] = valid[q] ? t - r * (r + 1) / 2 : 0;
+        int c = 0, rem = valid[q] ? t : 0;
+        while (rem >= TR - c) {
+            rem -= TR - c;
+            ++c;
+        }
+        tj[q] = c;
+        ti[q] = c + rem;
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -97,11 +105,12 @@ __global__ void __launch_bounds__(128, 4) chol_tiled_kernel(const float *A, int6
         float *pan = panel + (p & 1) * 4 * fp;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            float d = l[c][c];
-            if (!(d > 0.0f) && !fail) fail = 4 * p + c + 1;
-            d = sqrtf(fmaxf(d, 1e-30f));
-            const float rd = 1.0f / d;
-            l[c][c] = d;
+            const float d0 = l[c][c];
+            if (!(d0 > 0.0f) && !fail) fail = 4 * p + c + 1;
+            // one MUFU.RSQ gives both 1/sqrt(d) and sqrt(d) = d / sqrt(d) (serial chain)
+            const float dd = fmaxf(d0, 1e-30f);
+            const float rd = rsqrtf(dd);
+            l[c][c] = dd * rd;
 #pragma unroll
             for (int r = c + 1; r < 4; ++r) l[r][c] *= rd;
 #pragma unroll
