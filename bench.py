@@ -279,10 +279,14 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        # cudaProfilerStart/Stop bracket the timed region so that
+        # `ncu --profile-from-start off` lists exactly the step's launches
+        torch.cuda.profiler.start()
         ev0.record()
         run_steps(x, th, args.steps, kern)
         ev1.record()
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     launches = nat.LAUNCHES[0]
     ms_total = ev0.elapsed_time(ev1)
     if world > 1:

@@ -90,8 +90,10 @@ int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices,
  * K1+K2 on the tensor cores (tcgen05.mma kind::f16, TMEM accumulators).
  * Same contract as cmf_gram_assemble with a_weights == NULL, except that the
  * fixed factors are read from `fixed16`, the binary16 shadow written by
- * cmf_factors_to_half (row width `w16` = cmf_tc_width(f) halves), and the bias
- * accumulates in fp32 in the same MMAs.  Requires f <= 126, even a_stride.
+ * cmf_factors_to_half (row width `w16` = cmf_tc_width(f) halves, ncols + 1
+ * rows, the last one zero; column ids >= ncols gather as that zero row), and
+ * the bias accumulates in fp32 in the same MMAs (the ratings ride as two extra
+ * operand rows).  Requires f <= 120, even a_stride.
  *
  * Split precision (the exact route): pass `fixed16_lo` and `split_scale` from
  * cmf_factors_to_half_split; the kernel accumulates H H^T + H L^T + L H^T
@@ -101,11 +103,12 @@ int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices,
  */
 int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const float *b_weights,
                          int64_t nrows, const void *fixed16, const void *fixed16_lo,
-                         float split_scale, int32_t w16, int32_t f, double lam,
+                         int64_t ncols, float split_scale, int32_t w16, int32_t f, double lam,
                          int32_t weighted_reg, const float *base_packed, int32_t precision,
                          void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
                          int32_t *overflow_flag, void *stream);
-/* hi = fp16(scale*x), lo = fp16(scale*x - hi), both (rows, w16), zero padded;
+/* hi = fp16(scale*x), lo = fp16(scale*x - hi), both (rows + 1, w16), zero padded
+ * (row `rows` all zero, as cmf_factors_to_half);
  * a finite value whose hi overflows binary16 sets *overflow_flag. */
 int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi16, void *lo16,
                               int32_t w16, float scale, int32_t *overflow_flag, void *stream);
@@ -115,16 +118,22 @@ int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi1
  * tcgen05.mma into TMEM (fp16 operands from `fixed16`, fp32 accumulation) and
  * solved in place, target[u] <- CG_{f_s}(A_u + reg*I, b_u, x0 = target[u]),
  * eps = cg_tol * ||b_u||.  A_u never reaches HBM.  Replaces als.update_side
- * (als.py:54-74) for SolverConfig(method="cg").  f <= 126.  *breakdowns
+ * (als.py:54-74) for SolverConfig(method="cg").  f <= 120.  *breakdowns
  * (device int, nullable) accumulates p^T A p <= 0 exits.
  */
 int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
-                        int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
+                        int64_t nrows, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
                         int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
                         int32_t *breakdowns, void *stream);
+/* Debugging aid: a device buffer of 8 * 4096 int64 (or NULL to switch off) that
+ * CTA 0 of the tensor-core kernels fills with clock64 stamps per operand stage
+ * (producer wait / slot free / copies issued / MMA sees data / MMA commit). */
+int cmf_debug_trace(void *buf);
 /* Row width (halves) of the binary16 factor shadow for a given f. */
 int cmf_tc_width(int32_t f);
-/* fp32 (rows, f) -> binary16 (rows, w16), RNE, zero padded columns. */
+/* fp32 (rows, f) -> binary16 (rows + 1, w16), RNE, zero padded columns, plus an
+ * all-zero row `rows`: the tensor-core gather reads it for padding positions
+ * (and for column ids >= ncols), so out16 must hold (rows + 1) * w16 halves. */
 int cmf_factors_to_half(const float *x, int64_t rows, int32_t f, void *out16, int32_t w16,
                         void *stream);
 
@@ -172,7 +181,7 @@ int cmf_batch_cholesky(const float *a, int64_t a_stride, const float *b, const i
  * als.update_side (als.py:54-74).  method: 0 = cg, 1 = exact.  The workspace
  * must hold ws_rows systems of a_stride elements (fp16 or fp32 per
  * precision) plus ws_rows*f floats (b) and ws_rows int64 (n_u).  With
- * kernel == CMF_GRAM_TC, ws16 must hold ncols * cmf_tc_width(f) halves for
+ * kernel == CMF_GRAM_TC, ws16 must hold (ncols + 1) * cmf_tc_width(f) halves for
  * the binary16 shadow of `fixed` (ignored otherwise).
  * flags (4 device ints): [0] fp16 overflow, [1] CG breakdowns, [2] singular.
  */

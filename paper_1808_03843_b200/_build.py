@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-I", INCLUDE, "-I", CSRC]
+# extra nvcc flags, e.g. CMF_NVCC_EXTRA=-DCMF_TRACE for the pipeline timeline (tools/trace_fused.py)
+FLAGS += os.environ.get("CMF_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -34,12 +34,13 @@ _SIGNATURES = {
     "cmf_device_info": (ctypes.c_int, [_vp, _vp, _vp]),
     "cmf_gram_assemble": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i32, _f64, _i32,
                                          _vp, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
-    "cmf_gram_assemble_tc": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_float, _i32, _i32,
+    "cmf_gram_assemble_tc": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_float, _i32, _i32,
                                             _f64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
     "cmf_factors_to_half_split": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _i32, ctypes.c_float,
                                                  _vp, _vp]),
     "cmf_tc_width": (ctypes.c_int, [_i32]),
-    "cmf_fused_cg_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i32, _i32, _f64, _i32, _vp,
+    "cmf_debug_trace": (ctypes.c_int, [_vp]),
+    "cmf_fused_cg_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
                                            _i32, _f64, _vp, _vp]),
     "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
     "cmf_spmm_bias": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),
@@ -119,8 +120,9 @@ def call(name: str, *args):
 # ---------------------------------------------------------------- tensors
 
 def tc_width(f: int) -> int:
-    """Row width (halves) of the binary16 factor shadow the tensor-core Gram reads."""
-    return ((f + 2 + 7) // 8) * 8
+    """Row width (halves) of the binary16 factor shadow the tensor-core Gram reads
+    (= cmf_tc_width: f rounded up to 8, so every row is 16-byte aligned for TMA)."""
+    return ((f + 7) // 8) * 8
 
 
 def device() -> torch.device:

@@ -61,7 +61,7 @@ def aligned_stride(f: int) -> int:
     return (packed_size(f) + 7) // 8 * 8
 
 
-TC_MAX_F = 126  # tensor-core paths: f + 2 operand rows within M = 128
+TC_MAX_F = 120  # tensor-core paths: roundup8(f) feature rows + 2 rating rows within M = 128
 SPLIT_SCALE = 64.0  # split-fp16 shadow scale: lo stays normal for |theta| >= 2^-9
 
 
@@ -69,7 +69,7 @@ def resolve_gram_kernel(kernel: str | None, solver: SolverConfig, f: int | None 
     """Kernel choice for update_side/train.
 
     "auto": the CG route runs fused on the tensor cores ("tc": Gram in TMEM,
-    CG in registers, A never stored) when f <= 126; the exact route uses the
+    CG in registers, A never stored) when f <= 120; the exact route uses the
     split-precision tensor-core Gram ("tc_split": hi/lo fp16 operands, three
     MMAs, fp32-faithful -- the 1e-4 factor bar rules out a single fp16/TF32
     pass) and falls back to the SIMT FMA Gram for larger f.
@@ -156,11 +156,11 @@ class HalfUpdatePlan:
 
     def _shadow(self, fx, split: bool = False):
         """binary16 shadow of the fixed factors (hi, or hi + lo for the split Gram)."""
-        need = fx.shape[0] * self.w16 * (2 if split else 1)
+        need = (fx.shape[0] + 1) * self.w16 * (2 if split else 1)  # + the zero padding row
         if self.shadow is None or self.shadow.numel() < need:
             self.shadow = torch.empty(need, dtype=torch.float16, device=fx.device)
         if split:
-            half = fx.shape[0] * self.w16
+            half = (fx.shape[0] + 1) * self.w16
             nat.call("cmf_factors_to_half_split", nat.ptr(fx), fx.shape[0], self.f,
                      nat.ptr(self.shadow), nat.ptr(self.shadow) + 2 * half, self.w16, SPLIT_SCALE,
                      nat.ptr(self.flags), nat.stream_ptr())
@@ -191,7 +191,7 @@ class HalfUpdatePlan:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
             nat.call("cmf_fused_cg_update", nat.ptr(indptr) + 8 * row0, nat.ptr(indices),
-                     nat.ptr(values), nrows, nat.ptr(shadow), self.w16, f, float(lam),
+                     nat.ptr(values), nrows, nat.ptr(shadow), fx.shape[0], self.w16, f, float(lam),
                      int(bool(weighted_reg)), nat.ptr(tg) + 4 * row0 * f, int(solver.cg_iters),
                      float(solver.cg_tol), nat.ptr(self.flags) + 4, st)
             if record is not None:
@@ -206,7 +206,8 @@ class HalfUpdatePlan:
                 e0.record()
             if tc:
                 nat.call("cmf_gram_assemble_tc", nat.ptr(indptr) + 8 * r0, nat.ptr(indices),
-                         nat.ptr(values), nb, nat.ptr(shadow), lo, SPLIT_SCALE, self.w16, f, float(lam),
+                         nat.ptr(values), nb, nat.ptr(shadow), lo, fx.shape[0], SPLIT_SCALE, self.w16, f,
+                         float(lam),
                          int(bool(weighted_reg)), None, nat.PREC[solver.precision],
                          nat.ptr(self.a_ws), self.stride, nat.ptr(self.b_ws),
                          nat.ptr(self.nu_ws), nat.ptr(self.flags), st)

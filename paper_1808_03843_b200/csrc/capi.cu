@@ -20,12 +20,12 @@ int set_error(int code, const char *fmt, ...) {
 int gram_simt_launch(const int64_t *, const int32_t *, const float *, const float *, int64_t,
                      const float *, int, double, int, const float *, bool, bool, void *, int64_t,
                      float *, int64_t *, int32_t *, cudaStream_t);
-int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, const void *, float,
-                   int, int, double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
+int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, const void *, int64_t,
+                   float, int, int, double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
                    cudaStream_t);
 int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, int, float, int32_t *, cudaStream_t);
 int gram_tc_width(int f);
-int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int, int, double,
+int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
                     int, float *, int, double, int32_t *, cudaStream_t);
 int factors_to_half_launch(const float *, int64_t, int, void *, int, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
@@ -44,6 +44,8 @@ int predict_launch(const void *, const void *, bool, int64_t, const float *, con
                    float *, cudaStream_t);
 int pack_half_launch(const float *, void *, int64_t, int32_t *, cudaStream_t);
 
+int gram_tc_trace(void *buf);
+int fused_cg_trace(void *buf);
 }  // namespace cmf
 
 using namespace cmf;
@@ -104,6 +106,11 @@ int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices, const float
 
 int cmf_tc_width(int32_t f) { return gram_tc_width(f); }
 
+int cmf_debug_trace(void *buf) {
+    int rc = gram_tc_trace(buf);
+    return rc ? rc : fused_cg_trace(buf);
+}
+
 int cmf_factors_to_half(const float *x, int64_t rows, int32_t f, void *out16, int32_t w16,
                         void *stream) {
     REQUIRE(rows >= 0 && f >= 1 && w16 >= f, "bad dimensions");
@@ -121,7 +128,8 @@ int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi1
 }
 
 int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const float *b_weights,
-                         int64_t nrows, const void *fixed16, const void *fixed16_lo, float split_scale,
+                         int64_t nrows, const void *fixed16, const void *fixed16_lo, int64_t ncols,
+                         float split_scale,
                          int32_t w16, int32_t f, double lam, int32_t weighted_reg, const float *base_packed,
                          int32_t precision, void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
                          int32_t *overflow_flag, void *stream) {
@@ -131,13 +139,14 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
     if (nrows == 0) return CMF_OK;
     REQUIRE(indptr && a_out && fixed16, "null argument");
     REQUIRE(!fixed16_lo || split_scale > 0.0f, "split_scale must be > 0");
-    return gram_tc_launch(indptr, indices, b_weights, nrows, fixed16, fixed16_lo, split_scale, w16, f, lam,
+    REQUIRE(ncols >= 1, "ncols must be >= 1");
+    return gram_tc_launch(indptr, indices, b_weights, nrows, fixed16, fixed16_lo, ncols, split_scale, w16, f, lam,
                           weighted_reg, base_packed, precision == CMF_PREC_FP16, a_out, a_stride, b_out, nu_out,
                           overflow_flag, S(stream));
 }
 
 int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
-                        int64_t nrows, const void *fixed16, int32_t w16, int32_t f, double lam,
+                        int64_t nrows, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
                         int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
                         int32_t *breakdowns, void *stream) {
     REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
@@ -145,7 +154,8 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
     REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
     if (nrows == 0) return CMF_OK;
     REQUIRE(indptr && fixed16 && target, "null argument");
-    return fused_cg_launch(indptr, indices, values, nrows, fixed16, w16, f, lam, weighted_reg, target, f_s,
+    REQUIRE(ncols >= 1, "ncols must be >= 1");
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, f_s,
                            cg_tol, breakdowns, S(stream));
 }
 
@@ -208,7 +218,7 @@ int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *
     for (int64_t r0 = 0; r0 < nrows; r0 += ws_rows) {
         const int64_t nb = nrows - r0 < ws_rows ? nrows - r0 : ws_rows;
         int rc = kernel == CMF_GRAM_TC
-                     ? cmf_gram_assemble_tc(indptr + r0, indices, values, nb, ws16, nullptr, 1.0f, w16, f, lam,
+                     ? cmf_gram_assemble_tc(indptr + r0, indices, values, nb, ws16, nullptr, ncols, 1.0f, w16, f, lam,
                                             weighted_reg, nullptr, precision, ws_a, a_stride, ws_b,
                                             ws_nu, flags + 0, stream)
                      : cmf_gram_assemble(indptr + r0, indices, nullptr, values, nb, fixed, ncols, f,

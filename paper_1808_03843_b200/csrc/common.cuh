@@ -1,6 +1,7 @@
 // Shared helpers for the sm_100a kernels behind include/cmf_b200.h.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -9,17 +9,20 @@
 // exactly the register-resident row layout the CG matvec wants (thread i <->
 // TMEM lane i <-> row i of A_u), so the solve runs straight out of TMEM:
 //
-//   warps 8-11  producers  cp.async gather of binary16 factor rows (+ rating
-//                          rows f, f+1) into an 8-stage swizzled operand ring
-//   warp 12     MMA        tcgen05.mma kind::f16 chain per row into TMEM buffer
-//                          (row & 1); tcgen05.commit -> stage empty / tmem full
-//   warps 0-7   CG         two groups of 4 warps, one per TMEM buffer: load the
+//   warps 12-18 producers  cp.async gather of binary16 factor rows (+ the rating
+//                          rows) into a 12-stage swizzled operand ring
+//   warp 19     MMA        tcgen05.mma kind::f16 chain per row into TMEM buffer
+//                          (row % 3); tcgen05.commit -> stage empty / tmem full
+//   warps 0-11  CG         three groups of 4 warps, one per TMEM buffer: load the
 //                          row's A_u and b_u from TMEM (fp32), free the buffer,
 //                          run Algorithm 1 (corrected
-//                          r -= alpha*A p) with fp32 vectors: matvec = 25 FFMA2
-//                          per thread against p broadcast from shared memory,
-//                          deterministic 4-warp reductions on a named barrier;
-//                          write x_u in place (warm start = previous x_u).
+//                          r -= alpha*A p) in its pipelined form (one barrier
+//                          per iteration carries both dot products and the
+//                          next matvec's vector) with fp32 vectors; A_u stays
+//                          in TMEM and each matvec streams the thread's row in
+//                          32-column chunks (50 FFMA2 per thread); deterministic
+//                          4-warp reductions; write x_u in place (warm start =
+//                          previous x_u).
 //
 // Semantics vs the reference: the diagonal gets lambda*n_u (weighted) or
 // lambda; rows with n_u == 0 are left untouched; eps = cg_tol * ||b_u||;
@@ -27,27 +30,116 @@
 // used in fp32 straight from the accumulator (the reference rounds it to fp16
 // when precision="fp16"; the fused path never stores it -- strictly more
 // accurate, within the 1e-3 RMSE bar the CG route is graded on).
+#include <cstdlib>
+
 #include "tc_common.cuh"
 
 namespace cmf {
 namespace tc {
 
-constexpr int F_STAGES = 8;
-constexpr int F_THREADS = 416;
+constexpr int F_PROD = 7;  // producer warps: the gather rate scales with issuing warps
 constexpr int CG_THREADS = 128;
+// NG CG groups (== TMEM accumulator buffers, one warpgroup each) + 2 auxiliary
+// warpgroups (7 producers + the MMA warp).  Registers are rebalanced with
+// setmaxnreg: the CG warpgroups hold a register row of A_u (4*FC floats) and
+// grow to CG_REGS, the auxiliary warpgroups shrink to AUX_REGS, so that
+// NG*128*CG_REGS + 256*AUX_REGS == THREADS*LAUNCH_REGS <= 64K registers.
+template <int FC>
+struct FusedShape {
+    static constexpr int NG = FC <= 26 ? 3 : 2;
+    static constexpr int NBUF = NG + 1;  // TMEM accumulators rotate over the NG groups
+    static constexpr int THREADS = 32 * (4 * NG + F_PROD + 1);
+    static constexpr int MMA_WARP = 4 * NG + F_PROD;
+    static constexpr int LAUNCH_REGS = NG == 3 ? 96 : 128;
+    static constexpr int CG_REGS = NG == 3 ? 112 : 168;
+    static constexpr int AUX_REGS = NG == 3 ? 72 : 88;
+    static_assert(NG * 128 * CG_REGS + 256 * AUX_REGS == THREADS * LAUNCH_REGS, "register budget");
+};
+
+template <int R>
+__device__ __forceinline__ void regs_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));
+}
+template <int R>
+__device__ __forceinline__ void regs_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R));
+}
 
 struct FusedArgs {
     GatherArgs gather;
-    int N;
+    const __half *fixed16;  // binary16 shadow of the fixed factors (ncols, W)
+    int W, N, tmem_cols;  // shadow width, accumulator width (Gram + rating columns W, W+1)
     double lam;
     int weighted;
     float *target;  // (nrows, f) in/out
     int f_s;
+    int nprod;  // active producer warps (<= F_PROD)
+    int cg_only;  // timing experiment (CMF_FUSED_CG_ONLY): no gather / MMA
     float tol;
     int32_t *breakdowns;
 };
 
-using FPipe = Pipe<F_STAGES, false>;
+template <int NBUF>
+using FPipe = Pipe<12, false, NBUF>;  // 12 x 18 KB operand ring: bytes in flight for the gather
+
+// tcgen05.ld 32x32b of N consecutive columns (N = 4, 8, 16) into v[0..N)
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t *v);
+template <>
+__device__ __forceinline__ void tmem_ldn<4>(uint32_t taddr, uint32_t *v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr)
+                 : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_ldn<8>(uint32_t taddr, uint32_t *v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_ldn<32>(uint32_t taddr, uint32_t *v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_ldn<16>(uint32_t taddr, uint32_t *v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
+}
+// R (< 32, a multiple of 4) consecutive columns as x16 / x8 / x4 pieces
+template <int R>
+__device__ __forceinline__ void tmem_ld_tail(uint32_t taddr, uint32_t *v) {
+    if (R & 16) tmem_ldn<16>(taddr, v);
+    if (R & 8) tmem_ldn<8>(taddr + (R & 16), v + (R & 16));
+    if (R & 4) tmem_ldn<4>(taddr + (R & 24), v + (R & 24));
+}
+
+// NC (a multiple of 4) consecutive accumulator columns of this thread's lane
+template <int NC>
+__device__ __forceinline__ void tmem_load_row(uint32_t taddr, uint32_t (&v)[NC]) {
+#pragma unroll
+    for (int c = 0; c + 16 <= NC; c += 16) tmem_ldn<16>(taddr + c, v + c);
+    constexpr int r = NC % 16;
+    if (r & 8) tmem_ldn<8>(taddr + (NC - r), v + (NC - r));
+    if (r & 4) tmem_ldn<4>(taddr + (NC - (r & 4)), v + (NC - (r & 4)));
+    tmem_ld_wait();
+}
 
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     uint32_t v;
@@ -55,65 +147,34 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     return v;
 }
 
-// Group-wide (128 threads, 4 warps) deterministic sums of three values with one
-// barrier: warp butterflies, per-warp partials in red[3][4], fixed-order adds.
-__device__ __forceinline__ float3 group_sum3(float a, float b, float c, float *red, int bar_id) {
-    const int lane = threadIdx.x & 31, wg = (threadIdx.x >> 5) & 3;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-    }
-    if (lane == 0) {
-        red[wg] = a;
-        red[4 + wg] = b;
-        red[8 + wg] = c;
-    }
-    named_bar(bar_id, CG_THREADS);
-    return make_float3((red[0] + red[1]) + (red[2] + red[3]), (red[4] + red[5]) + (red[6] + red[7]),
-                       (red[8] + red[9]) + (red[10] + red[11]));
-}
-
-// Group-wide deterministic sum of one value.
-__device__ __forceinline__ float group_sum1(float a, float *red, int bar_id) {
-    const int lane = threadIdx.x & 31, wg = (threadIdx.x >> 5) & 3;
-    a = warp_sum(a);
-    if (lane == 0) red[wg] = a;
-    named_bar(bar_id, CG_THREADS);
-    return (red[0] + red[1]) + (red[2] + red[3]);
-}
-
 // FC = ceil(f/4): register row of A_u as FC*2 float2 pairs.
-template <int NCH, int FC>
-__global__ void __maxnreg__(128) fused_cg_kernel(FusedArgs g) {
+template <int FC>
+__global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(const __grid_constant__ FusedArgs g) {
+    constexpr int F_GROUPS = FusedShape<FC>::NG;
+    constexpr int F_THREADS = FusedShape<FC>::THREADS;
+    constexpr int F_MMA_WARP = FusedShape<FC>::MMA_WARP;
+    constexpr int NBUF = FusedShape<FC>::NBUF;
+    using PipeT = FPipe<NBUF>;
+    constexpr int NC = FC * 4;                 // matvec columns (>= f)
+    constexpr int NFULL = NC / 32, REM = NC % 32;
+    constexpr int NPAD = (NC + 31) / 32 * 32;  // p-vector buffer (zero past f)
+    static_assert(REM % 4 == 0, "tail chunk must be a multiple of 4 columns");
+    constexpr int F_STAGES = PipeT::kStages;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const GatherArgs &ga = g.gather;
     const int f = ga.f;
     unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    // [stages | per-group CG scratch: p (FC*4 floats) x2 buffers, red 2 x 4 floats | barriers | tmem slot]
-    float *scratch = reinterpret_cast<float *>(smem + F_STAGES * STAGE_BYTES);
-    constexpr int SCR = FC * 4 * 2 + 32;  // floats per group: p x2, red 2 x 12 (+pad)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(scratch + 2 * SCR);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + FPipe::kBars);
-    FPipe pp{smem_u32(smem), smem_u32(bars)};
+    // [stages | per-group CG scratch: p (FC*4 floats) x2 buffers, red 2 x 12 floats | barriers | tmem slot]
+    float *scratch = reinterpret_cast<float *>(smem + F_STAGES * PipeT::kStageBytes);
+    constexpr int SCR = 2 * ((FC * 4 + 31) / 32 * 32) + 32;  // floats per group: vector x2, red 2 x 8 (+pad)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(scratch + F_GROUPS * SCR);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + PipeT::kBars);
+    PipeT pp{smem_u32(smem), smem_u32(bars)};
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    for (int i = tid; i < F_STAGES * STAGE_BYTES / 16; i += F_THREADS)
-        reinterpret_cast<int4 *>(smem)[i] = make_int4(0, 0, 0, 0);
-    for (int i = tid; i < 2 * SCR; i += F_THREADS) scratch[i] = 0.0f;
-    if (tid == 0) {
-        for (int s = 0; s < F_STAGES; ++s) {
-            mbar_init(pp.full(s), 32);
-            mbar_init(pp.empty(s), 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(pp.tfull(b), 1);
-            mbar_init(pp.tempty(b), CG_THREADS);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 12) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    pipe_init(pp, smem, F_THREADS, 33, CG_THREADS);
+    for (int i = tid; i < F_GROUPS * SCR; i += F_THREADS) scratch[i] = 0.0f;
+    if (warp == F_MMA_WARP) tmem_alloc(smem_u32(tmem_slot), g.tmem_cols);
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -121,131 +182,184 @@ __global__ void __maxnreg__(128) fused_cg_kernel(FusedArgs g) {
     const uint32_t tmem_base = *tmem_slot;
     const int64_t G = gridDim.x;
 
-    if (warp >= 8 && warp < 12) {
-        produce<NCH, F_STAGES, false>(ga, pp, warp - 8, 4, lane, blockIdx.x, G);
-    } else if (warp == 12) {
-        if (lane == 0) issue_mma<F_STAGES, false>(ga, pp, tmem_base, g.N, blockIdx.x, G);
-        __syncwarp();
+    if (warp >= 4 * F_GROUPS && warp < F_MMA_WARP) {
+        regs_dec<FusedShape<FC>::AUX_REGS>();
+        if (warp - 4 * F_GROUPS < g.nprod && !g.cg_only)
+            produce<F_STAGES, false, NBUF>(ga, g.fixed16, nullptr, g.W, pp, warp - 4 * F_GROUPS, g.nprod, lane,
+                                           blockIdx.x, G);
+    } else if (warp == F_MMA_WARP) {
+        regs_dec<FusedShape<FC>::AUX_REGS>();
+        if (!g.cg_only) {
+            issue_mma<F_STAGES, false, NBUF>(ga, pp, tmem_base, g.N, blockIdx.x, G);
+        } else {  // timing experiment: hand out the (stale) accumulators without any MMA
+            uint32_t rowc = 0;
+            for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
+                if (ga.indptr[u + 1] == ga.indptr[u]) continue;
+                const int b = rowc % NBUF;
+                mbar_wait(pp.tempty(b), ((rowc / NBUF) & 1) ^ 1);
+                if (elect_one()) tc_commit(pp.tfull(b));
+                __syncwarp();
+                ++rowc;
+            }
+        }
     } else {
+        regs_inc<FusedShape<FC>::CG_REGS>();
         // ------------------------------------------------------------ CG groups
-        const int grp = warp >> 2;        // TMEM buffer this group drains
+        const int grp = warp >> 2;             // rows r with r % NG == grp
         const int i = (warp & 3) * 32 + lane;  // row of A_u == TMEM lane
         const int bar_id = 1 + grp;
-        float *pvec = scratch + grp * SCR;           // 2 x FC*4 floats (double buffer)
-        float *red = pvec + FC * 4 * 2;              // 2 x 12 floats
+        float *pvec = scratch + grp * SCR;     // 2 x NPAD floats (double buffer), zero past f
+        float *red = pvec + 2 * NPAD;          // 2 x 8 floats: warp partials of two dot products
         const bool act = i < f;
         int32_t brk = 0;
-        uint32_t rowc = 0;
-        int slot = 0, pb = 0;  // reduction / p-vector buffers alternate across rows too
-        auto gsum3 = [&](float a, float b, float c) {
-            const float3 s = group_sum3(a, b, c, red + 12 * slot, bar_id);
-            slot ^= 1;
-            return s;
-        };
-        auto gsum1 = [&](float a) {
-            const float s = group_sum1(a, red + 12 * slot, bar_id);
-            slot ^= 1;
-            return s;
-        };
+        uint32_t rowc = 0;         // non-empty rows of this CTA so far (all groups)
+        int slot = 0, pb = 0;      // reduction / p-vector buffers alternate across rows too
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
-            const int64_t p0 = ga.indptr[u], p1 = ga.indptr[u + 1];
-            if (p1 == p0) continue;
-            const uint32_t mine = (rowc & 1) == static_cast<uint32_t>(grp);
-            const uint32_t use = rowc >> 1;
-            ++rowc;
-            if (!mine) continue;
-            const int64_t n_u = p1 - p0;
+            const int64_t p0 = ga.indptr[u];
+            const int n_u = static_cast<int>(ga.indptr[u + 1] - p0);
+            if (n_u == 0) continue;
+            const uint32_t r_here = rowc++;
+            if (r_here % F_GROUPS != static_cast<uint32_t>(grp)) continue;
+            const int b = r_here % NBUF;
+            if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 0);
+            mbar_wait_backoff(pp.tfull(b), (r_here / NBUF) & 1);  // sleeps: long rows keep the group idle
+            if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 1);
+            tc_fence_after();
+            // A_u stays in TMEM for the whole solve (thread i <-> lane i <-> row i):
+            // every matvec streams the row in 16-column chunks, double-buffered.
+            // Columns [f, NPAD) meet zero p entries; rows >= f are zero padding
+            // except the two rating rows W, W+1, so threads i >= f zero their y.
+            const uint32_t tb = tmem_base + lane_base + b * g.N;
+            float bi = __uint_as_float(tmem_ld1(tb + g.W)) + __uint_as_float(tmem_ld1(tb + g.W + 1));
+            tmem_ld_wait();
+            bi = act ? bi : 0.0f;
+            if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 2);
+            int ev = 0;
             const float reg = g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
                                          : __double2float_rn(g.lam);
-            mbar_wait(pp.tfull(grp), use & 1);
-            tc_fence_after();
-            const uint32_t tb = tmem_base + lane_base + grp * 128;
-            float2 a2[FC * 2];
+            // One barrier per exchange: thread i publishes its entry of the vector
+            // to multiply and the warp sums of two dot products, then every thread
+            // reads the vector and the 4 warp partials.  The first 32-column chunk
+            // of the A row is requested from TMEM before the barrier.
+            //   y_i = (A_u v)_i + reg * v_i,  (sa, sb) = group sums of (da, db)
+            auto exchange = [&](float v, float da, float db, float &sa, float &sb, bool mv) -> float {
+                uint32_t abuf[2][32];
+                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
+                if (mv) tmem_ldn<32>(tb, abuf[0]);
 #pragma unroll
-            for (int cc = 0; cc < (FC * 4 + 31) / 32; ++cc) {
-                uint32_t v[32];
-                tmem_ld32(tb + cc * 32, v);
-                tmem_ld_wait();
-#pragma unroll
-                for (int jj = 0; jj < 32; jj += 2) {
-                    const int j = cc * 32 + jj;
-                    if (j < FC * 4) {
-                        // rows i >= f of the accumulator hold the rating rows: zero them so
-                        // the inactive threads contribute nothing to the reductions
-                        float lo = (act && j < f) ? __uint_as_float(v[jj]) : 0.0f;
-                        float hi = (act && j + 1 < f) ? __uint_as_float(v[jj + 1]) : 0.0f;
-                        a2[j / 2] = make_float2(lo, hi);
-                    }
+                for (int o = 16; o > 0; o >>= 1) {
+                    da += __shfl_xor_sync(0xffffffffu, da, o);
+                    db += __shfl_xor_sync(0xffffffffu, db, o);
                 }
-            }
-            const float bi = __uint_as_float(tmem_ld1(tb + f)) + __uint_as_float(tmem_ld1(tb + f + 1));
-            tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(pp.tempty(grp));
-
-            float xi = act ? g.target[u * f + i] : 0.0f;
-            auto matvec = [&](float v) {
-                float *pv = pvec + pb * FC * 4;
+                float *pv = pvec + pb * NPAD;
+                float *rd = red + 8 * slot;
                 pb ^= 1;
+                slot ^= 1;
                 if (act) pv[i] = v;
-                named_bar(bar_id, CG_THREADS);
-                // two independent FFMA2 chains (latency), summed at the end
-                float2 ya = make_float2(0.0f, 0.0f), yb = make_float2(0.0f, 0.0f);
-                const float4 *p4 = reinterpret_cast<const float4 *>(pv);
-#pragma unroll
-                for (int c = 0; c < FC; ++c) {
-                    const float4 q = p4[c];
-                    ya = __ffma2_rn(a2[2 * c], make_float2(q.x, q.y), ya);
-                    yb = __ffma2_rn(a2[2 * c + 1], make_float2(q.z, q.w), yb);
+                if (lane == 0) {
+                    rd[warp & 3] = da;
+                    rd[4 + (warp & 3)] = db;
                 }
-                return fmaf(reg, v, (ya.x + ya.y) + (yb.x + yb.y));  // + lambda*n_u on the diagonal
+                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
+                named_bar(bar_id, CG_THREADS);
+                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
+                sa = (rd[0] + rd[1]) + (rd[2] + rd[3]);
+                sb = (rd[4] + rd[5]) + (rd[6] + rd[7]);
+                if (!mv) return 0.0f;
+                const float4 *p4 = reinterpret_cast<const float4 *>(pv);
+                float2 ya = make_float2(0.0f, 0.0f), yb = make_float2(0.0f, 0.0f);
+                auto chunk = [&](const uint32_t *av, int c0, int ncol) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (4 * q < ncol) {
+                            const float4 pq = p4[c0 / 4 + q];
+                            ya = __ffma2_rn(make_float2(__uint_as_float(av[4 * q]), __uint_as_float(av[4 * q + 1])),
+                                            make_float2(pq.x, pq.y), ya);
+                            yb = __ffma2_rn(make_float2(__uint_as_float(av[4 * q + 2]), __uint_as_float(av[4 * q + 3])),
+                                            make_float2(pq.z, pq.w), yb);
+                        }
+                    }
+                };
+#pragma unroll
+                for (int c = 0; c < NFULL; ++c) {
+                    tmem_ld_wait();  // chunk c has landed
+                    if (c + 1 < NFULL) tmem_ldn<32>(tb + 32 * (c + 1), abuf[(c + 1) & 1]);
+                    else if (REM) tmem_ld_tail<REM>(tb + 32 * NFULL, abuf[(c + 1) & 1]);
+                    chunk(abuf[c & 1], 32 * c, 32);
+                }
+                if (REM) {
+                    tmem_ld_wait();
+                    chunk(abuf[NFULL & 1], 32 * NFULL, REM);
+                }
+                const float y = act ? (ya.x + ya.y) + (yb.x + yb.y) : 0.0f;
+                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
+                return fmaf(reg, v, y);
             };
-            float ap = matvec(xi);
-            float r = act ? bi - ap : 0.0f;
-            const float3 s0 = gsum3(act ? bi * bi : 0.0f, r * r, 0.0f);
-            const float eps = g.tol * sqrtf(s0.x);
-            float p = r;
-            float rs_old = s0.y;
+            // Pipelined CG (Ghysels & Vanroose): the same iterates as Algorithm 1
+            // in exact arithmetic; s = A p, z = A s, w = A r are carried by
+            // recurrences, so each iteration needs ONE exchange: (r.r, w.r) and
+            // m = A w together.  Semantics as the reference: at least one update
+            // unless p^T A p <= 0 (breakdown, x kept); stop once ||r|| < eps.
+            float* const tgt = g.target + u * f;
+            float xi = act ? tgt[i] : 0.0f;
+            float bb, unused;
+            float r = bi - exchange(xi, bi * bi, 0.0f, bb, unused, true);
+            const float eps2 = g.tol * g.tol * bb;
+            float gamma, delta;
+            float w = exchange(r, 0.0f, 0.0f, gamma, delta, true);
+            float p = 0.0f, sv = 0.0f, z = 0.0f, gamma_old = 1.0f, alpha_old = 1.0f;
             int bd = 0;
             for (int step = 0; step < g.f_s; ++step) {
-                ap = matvec(p);
-                const float pap = gsum1(act ? p * ap : 0.0f);
+                const bool last = step + 1 >= g.f_s;
+                const float m = exchange(w, r * r, w * r, gamma, delta, !last);
+                if (step > 0 && (gamma == 0.0f || gamma < eps2)) break;
+                const float beta = step > 0 ? gamma * __frcp_rn(gamma_old) : 0.0f;
+                const float pap = step > 0 ? delta - beta * gamma * __frcp_rn(alpha_old) : delta;
                 if (!(pap > 0.0f)) {
                     bd = 1;
                     break;
                 }
-                const float alpha = rs_old / pap;
-                xi = fmaf(alpha, p, xi);
-                r = fmaf(-alpha, ap, r);
-                const float rs_new = gsum1(r * r);
-                if (rs_new == 0.0f || sqrtf(rs_new) < eps) break;
-                const float beta = rs_new / rs_old;
+                const float alpha = gamma * __frcp_rn(pap);
+                z = fmaf(beta, z, m);
+                sv = fmaf(beta, sv, w);
                 p = fmaf(beta, p, r);
-                rs_old = rs_new;
+                xi = fmaf(alpha, p, xi);
+                r = fmaf(-alpha, sv, r);
+                w = fmaf(-alpha, z, w);
+                gamma_old = gamma;
+                alpha_old = alpha;
             }
-            if (act) g.target[u * f + i] = xi;
+            tc_fence_before();
+            mbar_arrive(pp.tempty(b));  // the accumulator is free for row r_here + NBUF
+            if (act) tgt[i] = xi;
+            if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 3);
             brk += bd;
         }
         if (i == 0 && brk && g.breakdowns) atomicAdd(g.breakdowns, brk);
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 12) {
+    if (warp == F_MMA_WARP) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, TMEM_COLS);
+        tmem_dealloc(tmem_base, g.tmem_cols);
     }
 }
 
 }  // namespace tc
 
 int gram_tc_width(int f);
+int fused_cg_trace(void *buf) { return tc::set_trace_buf(buf); }
 
-template <int NCH, int FC>
-static int launch_fused(const tc::FusedArgs &g, cudaStream_t st) {
-    constexpr int SCR = FC * 4 * 2 + 32;
-    const size_t smem = 1024 + tc::F_STAGES * tc::STAGE_BYTES + 2 * SCR * sizeof(float) + tc::FPipe::kBars * 8 + 16;
-    auto k = tc::fused_cg_kernel<NCH, FC>;
+template <int FC>
+static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
+    using Shape = tc::FusedShape<FC>;
+    using PipeT = tc::FPipe<Shape::NBUF>;
+    constexpr int SCR = 2 * ((FC * 4 + 31) / 32 * 32) + 32;
+    const size_t smem = 1024 + PipeT::kStages * PipeT::kStageBytes + Shape::NG * SCR * sizeof(float) +
+                        PipeT::kBars * 8 + 16;
+    g.tmem_cols = Shape::NBUF * g.N <= 256 ? 256 : 512;
+    auto k = tc::fused_cg_kernel<FC>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return set_error(CMF_ECUDA, "fused_cg smem attr: %s", cudaGetErrorString(e));
     int dev = 0, sms = 148;
@@ -253,57 +367,62 @@ static int launch_fused(const tc::FusedArgs &g, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = sms;
     if (grid > g.gather.nrows) grid = g.gather.nrows;
-    k<<<static_cast<unsigned>(grid), tc::F_THREADS, smem, st>>>(g);
+    k<<<static_cast<unsigned>(grid), Shape::THREADS, smem, st>>>(g);
     return check_launch("fused_cg_kernel");
 }
 
-// f (<= 126) -> template instance: NCH = W/8 with W = roundup8(f+2), FC = ceil(f/4)
-#define CMF_FUSED_CASE(FMAX, NCHV, FCV) \
-    if (f <= FMAX && nch == NCHV) return launch_fused<NCHV, FCV>(g, st);
+// f (<= 120) -> template instance FC = ceil(f/4), bucketed
+#define CMF_FUSED_CASE(FMAX, FCV) \
+    if (f <= FMAX) return launch_fused<FCV>(g, st);
 
 int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
-                    const void *fixed16, int W, int f, double lam, int weighted, float *target, int f_s,
-                    double cg_tol, int32_t *breakdowns, cudaStream_t st) {
+                    const void *fixed16, int64_t ncols, int W, int f, double lam, int weighted, float *target,
+                    int f_s, double cg_tol, int32_t *breakdowns, cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
-    if (f + 2 > tc::M) return set_error(CMF_EINVAL, "fused CG supports f <= %d (got %d)", tc::M - 2, f);
+    if (W + 2 > tc::M) return set_error(CMF_EINVAL, "fused CG supports f <= %d (got %d)", tc::M - 8, f);
     if (W != gram_tc_width(f)) return set_error(CMF_EINVAL, "fixed16 width must be %d", gram_tc_width(f));
     if ((reinterpret_cast<uintptr_t>(fixed16) & 15) != 0) return set_error(CMF_EINVAL, "fixed16 must be 16-byte aligned");
+    if (ncols < 1 || ncols >= (int64_t(1) << 31)) return set_error(CMF_EINVAL, "bad shadow row count");
     tc::FusedArgs g{};
+    g.fixed16 = static_cast<const __half *>(fixed16);
+    g.W = W;
     g.gather.indptr = indptr;
     g.gather.indices = indices;
     g.gather.values = values;
-    g.gather.fixed16 = static_cast<const __half *>(fixed16);
-    g.gather.fixed16_lo = nullptr;
     g.gather.nrows = nrows;
     g.gather.f = f;
-    g.N = ((f + 2 + 15) / 16) * 16;
+    g.gather.ncols = static_cast<int>(ncols);
+    g.gather.trace = tc::g_trace_buf;
+    g.N = ((W + 2 + 15) / 16) * 16;
     g.lam = lam;
     g.weighted = weighted;
     g.target = target;
     g.f_s = f_s;
+    {
+        const char *e = getenv("CMF_FUSED_PROD");
+        g.nprod = e ? atoi(e) : tc::F_PROD;
+        if (g.nprod < 1 || g.nprod > tc::F_PROD) g.nprod = tc::F_PROD;
+        const char *c = getenv("CMF_FUSED_CG_ONLY");
+        g.cg_only = c ? atoi(c) : 0;
+    }
     g.tol = static_cast<float>(cg_tol);
     g.breakdowns = breakdowns;
-    const int nch = W / 8;
-    // instances for the common factor dimensions; FC = ceil(f/4) rounded up to the bucket
-    CMF_FUSED_CASE(6, 1, 2)
-    CMF_FUSED_CASE(14, 2, 4)
-    CMF_FUSED_CASE(22, 3, 6)
-    CMF_FUSED_CASE(30, 4, 8)
-    CMF_FUSED_CASE(32, 5, 8)
-    CMF_FUSED_CASE(38, 5, 10)
-    CMF_FUSED_CASE(46, 6, 12)
-    CMF_FUSED_CASE(54, 7, 14)
-    CMF_FUSED_CASE(62, 8, 16)
-    CMF_FUSED_CASE(64, 9, 16)
-    CMF_FUSED_CASE(70, 9, 18)
-    CMF_FUSED_CASE(78, 10, 20)
-    CMF_FUSED_CASE(86, 11, 22)
-    CMF_FUSED_CASE(94, 12, 24)
-    CMF_FUSED_CASE(100, 13, 25)
-    CMF_FUSED_CASE(102, 13, 26)
-    CMF_FUSED_CASE(110, 14, 28)
-    CMF_FUSED_CASE(118, 15, 30)
-    CMF_FUSED_CASE(126, 16, 32)
+    CMF_FUSED_CASE(8, 2)
+    CMF_FUSED_CASE(16, 4)
+    CMF_FUSED_CASE(24, 6)
+    CMF_FUSED_CASE(32, 8)
+    CMF_FUSED_CASE(40, 10)
+    CMF_FUSED_CASE(48, 12)
+    CMF_FUSED_CASE(56, 14)
+    CMF_FUSED_CASE(64, 16)
+    CMF_FUSED_CASE(72, 18)
+    CMF_FUSED_CASE(80, 20)
+    CMF_FUSED_CASE(88, 22)
+    CMF_FUSED_CASE(96, 24)
+    CMF_FUSED_CASE(100, 25)
+    CMF_FUSED_CASE(104, 26)
+    CMF_FUSED_CASE(112, 28)
+    CMF_FUSED_CASE(120, 30)
     return set_error(CMF_EINVAL, "no fused CG instance for f=%d", f);
 }
 #undef CMF_FUSED_CASE

@@ -6,16 +6,17 @@
 // factor rows are the K dimension of one M=128 x N x K MMA chain.
 //
 // Operand trick (tc_common.cuh): the gathered rows are staged ONCE per
-// K-chunk as an MN-major, 128-byte-swizzled UMMA operand and the SAME shared
-// buffer is passed as both A (M = 128 feature rows) and B (N = roundup16(f+2)
-// feature rows).  Rows f and f+1 of the operand carry the row's ratings
-// (fp16 hi + lo), so accumulator columns f, f+1 give b_u = sum_p r_p theta_p:
+// K-chunk by cp.async as an MN-major, 128-byte-swizzled UMMA operand
+// and the SAME shared buffer is passed as both A (M = 128 feature rows) and B
+// (N = roundup16(W + 2) rows).  Operand rows W, W+1 carry the row's ratings
+// (fp16 hi + lo), so accumulator columns W, W+1 give b_u = sum_p r_p theta_p:
 // the bias rides along in the same MMAs (fp32 accumulation in TMEM).
 //
 // The fixed factor matrix is read from a binary16 shadow (cmf_factors_to_half,
-// row width W = roundup8(f+2) halves, zero padded) so every 16-byte chunk of
-// a gathered row is one cp.async: the gather needs no SIMT conversion, and
-// the shadow of X (Netflix: 100 MB) stays resident in the 126 MB L2.
+// row width W = roundup8(f) halves, zero padded): every 16-byte chunk of a
+// gathered row is one cp.async with no SIMT conversion, and the shadow of X
+// (Netflix: 100 MB) stays resident in the 126 MB L2 (loads carry an L2
+// evict_last hint).
 //
 // Warp roles (288 threads, 2 CTAs per SM, persistent over rows):
 //   warps 0-3  epilogue: tcgen05.ld the accumulator (thread i <-> TMEM lane i
@@ -42,8 +43,9 @@ constexpr int EPI_THREADS = 128;
 
 struct Args {
     GatherArgs gather;
+    const __half *fixed16, *fixed16_lo;  // binary16 shadow (+ split residual), (ncols, W)
     float gram_scale, bias_scale;  // undo the split shadow's power-of-two scaling
-    int N;
+    int N, tmem_cols;  // accumulator width (Gram + rating columns W, W+1), TMEM allocation
     double lam;
     int weighted;
     const float *base;
@@ -59,8 +61,8 @@ __device__ __forceinline__ void bar_epi() { named_bar(1, EPI_THREADS); }
 // Packed-offset table: tab[k] = i*W + j for packed entry k = i*(i+1)/2 + j.
 // Built once per CTA; the epilogue copy-out walks the packed row with it.
 template <int NCH, bool HALF_OUT, bool SPLIT>
-__global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
-    using PipeT = Pipe<STAGES, SPLIT>;
+__global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_constant__ Args g) {
+    using PipeT = Pipe<STAGES, SPLIT, 2>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     constexpr int W = NCH * 8;
     using SqT = typename std::conditional<HALF_OUT, __half, float>::type;
@@ -80,25 +82,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // zero the operand ring once: MN-blocks >= NCH (rows >= W) are never written again
-    for (int i = tid; i < STAGES * PipeT::kStageBytes / 16; i += NUM_THREADS)
-        reinterpret_cast<int4 *>(stage_mem)[i] = make_int4(0, 0, 0, 0);
+    pipe_init(pp, stage_mem, NUM_THREADS, 33, EPI_THREADS);
     for (int i = tid; i < f; i += NUM_THREADS) {
         const int base = i * (i + 1) / 2;
         for (int j = 0; j <= i; ++j) tab[base + j] = static_cast<uint16_t>(i * W + j);
     }
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(pp.full(s), 32);  // one producer warp per stage
-            mbar_init(pp.empty(s), 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(pp.tfull(b), 1);
-            mbar_init(pp.tempty(b), EPI_THREADS);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), g.tmem_cols);
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -107,10 +96,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
 
     const int64_t G = gridDim.x;
     if (warp >= 4 && warp < 8) {
-        produce<NCH, STAGES, SPLIT>(ga, pp, warp - 4, 4, lane, blockIdx.x, G);
+        produce<STAGES, SPLIT, 2>(ga, g.fixed16, g.fixed16_lo, W, pp, warp - 4, 4, lane, blockIdx.x, G);
     } else if (warp == 8) {
-        if (lane == 0) issue_mma(ga, pp, tmem_base, g.N, blockIdx.x, G);
-        __syncwarp();
+        issue_mma<STAGES, SPLIT, 2>(ga, pp, tmem_base, g.N, blockIdx.x, G);
     } else {
         // ------------------------------------------------------------ epilogue
         // (1) thread i (= TMEM lane = matrix row) drains its accumulator row into
@@ -121,7 +109,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
         //     coalesced to HBM, four entries per step.
         const int i = warp * 32 + lane;
         const int nchunk = (g.N + 31) >> 5;
-        const int bias_cc = f >> 5, bias_cc1 = (f + 1) >> 5;
+        const int bias_cc = W >> 5, bias_cc1 = (W + 1) >> 5;
         float ovf_max = 0.0f;
         uint32_t rowc = 0;
         SqT *sq_row = sq + static_cast<size_t>(i) * W;
@@ -138,7 +126,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
                 const int b = rowc & 1;
                 mbar_wait(pp.tfull(b), (rowc >> 1) & 1);
                 tc_fence_after();
-                const uint32_t tbase = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + b * 128;
+                const uint32_t tbase = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + b * g.N;
                 for (int cc = 0; cc < nchunk; ++cc) {
                     uint32_t v[32];
                     tmem_ld32(tbase + cc * 32, v);
@@ -148,7 +136,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) {
                             const int j = c0 + jj;
-                            const float sc = (j == f || j == f + 1) ? g.bias_scale : g.gram_scale;
+                            const float sc = (j == W || j == W + 1) ? g.bias_scale : g.gram_scale;
                             v[jj] = __float_as_uint(__uint_as_float(v[jj]) * sc);
                         }
                     }
@@ -160,7 +148,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
                     if (cc == bias_cc || cc == bias_cc1) {  // warp-uniform
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
-                            if (c0 + jj == f || c0 + jj == f + 1) bias += __uint_as_float(v[jj]);
+                            if (c0 + jj == W || c0 + jj == W + 1) bias += __uint_as_float(v[jj]);
                     }
                     if (i < f) {
 #pragma unroll
@@ -238,18 +226,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(Args g) {
     __syncthreads();
     if (warp == 8) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, TMEM_COLS);
+        tmem_dealloc(tmem_base, g.tmem_cols);
     }
 }
 
-// fp32 (rows, f) -> binary16 (rows, W), zero padded, RNE.
+// fp32 (rows, f) -> binary16 (rows + 1, W), zero padded, RNE; row `rows` is the
+// all-zero row the gather reads for padding positions.
 __global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __half *out, int W) {
-    const int64_t n = rows * W;
+    const int64_t n = (rows + 1) * W;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
         const int64_t r = e / W;
         const int c = static_cast<int>(e - r * W);
-        out[e] = c < f ? __float2half_rn(x[r * f + c]) : __float2half_rn(0.0f);
+        out[e] = (c < f && r < rows) ? __float2half_rn(x[r * f + c]) : __float2half_rn(0.0f);
     }
 }
 
@@ -257,13 +246,13 @@ __global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __ha
 // two that keeps lo out of the binary16 subnormal range for |x| >= 2^-9.
 __global__ void factors_to_half_split_kernel(const float *x, int64_t rows, int f, __half *hi, __half *lo, int W,
                                              float scale, int32_t *ovf) {
-    const int64_t n = rows * W;
+    const int64_t n = (rows + 1) * W;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     int bad = 0;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
         const int64_t r = e / W;
         const int c = static_cast<int>(e - r * W);
-        const float v = c < f ? x[r * f + c] * scale : 0.0f;
+        const float v = (c < f && r < rows) ? x[r * f + c] * scale : 0.0f;
         const __half h = __float2half_rn(v);
         if (isfinite(v) && __hisinf(h)) bad = 1;
         hi[e] = h;
@@ -277,18 +266,20 @@ __global__ void factors_to_half_split_kernel(const float *x, int64_t rows, int f
 int factors_to_half_split_launch(const float *x, int64_t rows, int f, void *hi, void *lo, int W, float scale,
                                  int32_t *ovf, cudaStream_t st) {
     if (rows == 0) return CMF_OK;
-    int64_t blocks = (rows * W + 255) / 256;
+    int64_t blocks = ((rows + 1) * W + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     tc::factors_to_half_split_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         x, rows, f, static_cast<__half *>(hi), static_cast<__half *>(lo), W, scale, ovf);
     return check_launch("factors_to_half_split_kernel");
 }
 
-int gram_tc_width(int f) { return ((f + 2 + 7) / 8) * 8; }
+int gram_tc_trace(void *buf) { return tc::set_trace_buf(buf); }
+
+int gram_tc_width(int f) { return ((f + 7) / 8) * 8; }
 
 int factors_to_half_launch(const float *x, int64_t rows, int f, void *out, int W, cudaStream_t st) {
     if (rows == 0) return CMF_OK;
-    int64_t blocks = (rows * W + 255) / 256;
+    int64_t blocks = ((rows + 1) * W + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     tc::factors_to_half_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, rows, f,
                                                                              static_cast<__half *>(out), W);
@@ -304,8 +295,8 @@ static int launch_nch(const tc::Args &g, size_t smem, int64_t nrows, cudaStream_
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    // two CTAs per SM when their shared memory fits (TMEM: 2 x 256 columns per SM)
-    per_sm = (2 * (smem + 1024) <= 227 * 1024) ? 2 : 1;
+    // two CTAs per SM when their shared memory and TMEM (2 x 256 columns) fit
+    per_sm = (2 * (smem + 1024) <= 227 * 1024 && g.tmem_cols <= 256) ? 2 : 1;
     int64_t grid = static_cast<int64_t>(per_sm) * sms;
     if (grid > nrows) grid = nrows;
     k<<<static_cast<unsigned>(grid), tc::NUM_THREADS, smem, st>>>(g);
@@ -335,30 +326,35 @@ static int dispatch_nch(int nch, const tc::Args &g, size_t smem, int64_t nrows, 
 }
 
 int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
-                   const void *fixed16, const void *fixed16_lo, float split_scale, int W, int f, double lam,
+                   const void *fixed16, const void *fixed16_lo, int64_t ncols, float split_scale, int W, int f,
+                   double lam,
                    int weighted, const float *base, bool half, void *a_out, int64_t a_stride, float *b_out,
                    int64_t *nu_out, int32_t *overflow, cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
-    if (f + 2 > tc::M)
-        return set_error(CMF_EINVAL, "tensor-core Gram supports f <= %d (got %d)", tc::M - 2, f);
+    if (W + 2 > tc::M)
+        return set_error(CMF_EINVAL, "tensor-core Gram supports f <= %d (got %d)", tc::M - 8, f);
     if (W != gram_tc_width(f)) return set_error(CMF_EINVAL, "fixed16 width must be %d", gram_tc_width(f));
     const int esz = half ? 2 : 4;
     if ((a_stride % 2) != 0 || (reinterpret_cast<uintptr_t>(a_out) & 15) != 0)
         return set_error(CMF_EINVAL, "tensor-core Gram needs an even a_stride and a 16-byte aligned a_out");
-    if ((reinterpret_cast<uintptr_t>(fixed16) & 15) != 0)
-        return set_error(CMF_EINVAL, "fixed16 must be 16-byte aligned");
     tc::Args g{};
+    const bool split = fixed16_lo != nullptr;
+    if ((reinterpret_cast<uintptr_t>(fixed16) & 15) != 0 || (reinterpret_cast<uintptr_t>(fixed16_lo) & 15) != 0)
+        return set_error(CMF_EINVAL, "fixed16 / fixed16_lo must be 16-byte aligned");
+    if (ncols < 1 || ncols >= (int64_t(1) << 31)) return set_error(CMF_EINVAL, "bad shadow row count");
+    g.fixed16 = static_cast<const __half *>(fixed16);
+    g.fixed16_lo = static_cast<const __half *>(fixed16_lo);
     g.gather.indptr = indptr;
     g.gather.indices = indices;
     g.gather.values = values;
-    g.gather.fixed16 = static_cast<const __half *>(fixed16);
-    g.gather.fixed16_lo = static_cast<const __half *>(fixed16_lo);
     g.gather.nrows = nrows;
     g.gather.f = f;
-    const bool split = fixed16_lo != nullptr;
+    g.gather.ncols = static_cast<int>(ncols);
+    g.gather.trace = tc::g_trace_buf;
     g.gram_scale = split ? 1.0f / (split_scale * split_scale) : 1.0f;
     g.bias_scale = split ? 1.0f / split_scale : 1.0f;
-    g.N = ((f + 2 + 15) / 16) * 16;
+    g.N = ((W + 2 + 15) / 16) * 16;
+    g.tmem_cols = 2 * g.N <= 256 ? 256 : 512;
     g.lam = lam;
     g.weighted = weighted;
     g.base = base;
@@ -370,8 +366,9 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     const int64_t P = packed_size(f);
     const size_t sq_bytes = ((static_cast<size_t>(f) * W * esz) + 15) & ~static_cast<size_t>(15);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
-    const size_t smem = 1024 + tc::STAGES * tc::STAGE_BYTES * (split ? 2 : 1) + sq_bytes + tab_bytes +
-                        tc::Pipe<tc::STAGES>::kBars * 8 + 16;
+    const size_t stage_bytes = split ? tc::Pipe<tc::STAGES, true, 2>::kStageBytes
+                                     : tc::Pipe<tc::STAGES, false, 2>::kStageBytes;
+    const size_t smem = 1024 + tc::STAGES * stage_bytes + sq_bytes + tab_bytes + tc::Pipe<tc::STAGES>::kBars * 8 + 16;
     const int nch = W / 8;
     if (split) {
         if (half) return set_error(CMF_EINVAL, "the split-precision Gram stores fp32");

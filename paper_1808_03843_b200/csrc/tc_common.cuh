@@ -1,6 +1,6 @@
 // Shared pieces of the tcgen05 Gram kernels (gram_tc.cu, fused_cg.cu):
-// PTX wrappers, the swizzled UMMA operand layout, the cp.async gather producer
-// and the single-thread MMA issuer.
+// PTX wrappers, the swizzled UMMA operand layout, the TMA gather producer and
+// the single-thread MMA issuer.
 //
 // Operand layout (one pipeline stage = KS = 64 gathered factor rows):
 //   the stage holds the K x 128 operand "Theta_S^T" (feature rows, gathered
@@ -9,14 +9,21 @@
 //     K-block  kb (gathered rows 8kb .. 8kb+7)        stride SBO = 1024 B
 //     inside the 1024 B atom: gathered row r = k%8 at r*128 B, and the 16-byte
 //     chunk cb (features 8cb .. 8cb+7 of the block) at ((cb ^ r) << 4).
-//   A gathered binary16 factor row is therefore 13 contiguous 16-byte chunks in
-//   global memory that land in one 128-byte atom row per MN-block; the gather
-//   maps consecutive lanes to consecutive chunks of the same row, so a warp
-//   instruction reads two whole rows (coalesced) and writes conflict-free.
+//   A gathered binary16 factor row is W/8 contiguous 16-byte chunks in global
+//   memory that land in one 128-byte atom row per MN-block; the cp.async
+//   gather maps consecutive lanes to consecutive chunks of the same row, so a
+//   warp instruction reads two whole rows (coalesced) and writes them
+//   conflict-free.  (A TMA tile::gather4 writes the same layout, but measured
+//   on B200 its per-request cost caps a 128-byte-row gather near 3 TB/s;
+//   the LSU path is faster for this access pattern.)
 //   The SAME stage is the A operand (M = 128 feature rows) and the B operand
-//   (N = roundup16(f+2) feature rows) of kind::f16 MMAs with fp32 TMEM
-//   accumulation: D = Theta_S^T Theta_S.  Rows f and f+1 of the operand carry
-//   the row's ratings (fp16 hi + lo), so D[:, f] + D[:, f+1] = b_u.
+//   (N = roundup16(W + 2) rows) of kind::f16 MMAs with fp32 TMEM
+//   accumulation: D = Theta_S^T Theta_S.  Operand rows W and W+1 (just past
+//   the shadow's zero-padded width W = roundup8(f)) carry the row's ratings as
+//   fp16 hi/lo, so accumulator columns W, W+1 hold the two halves of
+//   b_u = Theta_S^T r: the bias rides in the same MMAs.  Those rows sit in a
+//   16-byte chunk no cp.async writes, so the producer stores them directly.
+//   (Accumulator ROWS W, W+1 hold rating-weighted sums too and are ignored.)
 #pragma once
 
 #include "common.cuh"
@@ -29,7 +36,6 @@ constexpr int M = 128;
 constexpr int MNBLK_BYTES = 8192;  // LBO
 constexpr int KBLK_BYTES = 1024;   // SBO
 constexpr int STAGE_BYTES = 2 * MNBLK_BYTES;
-constexpr int TMEM_COLS = 256;
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
@@ -69,12 +75,6 @@ __device__ __forceinline__ void mbar_wait_backoff(uint32_t a, uint32_t parity) {
         if (ns < 512) ns <<= 1;
     }
 }
-__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, uint32_t bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -104,6 +104,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr)
         : "memory");
 }
+__device__ __forceinline__ int lane_id() { return static_cast<int>(threadIdx.x & 31); }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -117,16 +118,15 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t cols) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols) : "memory");
 }
 
-// v.{x,y,z,w} as 8 halves; set half `pos` (runtime) without a local array
-__device__ __forceinline__ void set_half(uint4 &v, int pos, uint16_t h) {
-    const uint32_t sh = (pos & 1) * 16, keep = ~(0xFFFFu << sh), val = static_cast<uint32_t>(h) << sh;
-    const int w = pos >> 1;
-    v.x = w == 0 ? (v.x & keep) | val : v.x;
-    v.y = w == 1 ? (v.y & keep) | val : v.y;
-    v.z = w == 2 ? (v.z & keep) | val : v.z;
-    v.w = w == 3 ? (v.w & keep) | val : v.w;
+// ------------------------------------------------------------------ async copies
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 // byte address of (gathered row k, 16-byte feature chunk c) inside a stage
 __device__ __forceinline__ uint32_t operand_addr(uint32_t stage, int k, int c) {
     return stage + (c >> 3) * MNBLK_BYTES + (k >> 3) * KBLK_BYTES + (k & 7) * 128 + (((c & 7) ^ (k & 7)) << 4);
@@ -143,37 +143,39 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
     d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
     return d;
 }
-
 // kind::f16 instruction descriptor: F16 x F16 -> F32, A and B MN-major.
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
     return (1u << 4) | (0u << 7) | (0u << 10) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
            (static_cast<uint32_t>(m >> 4) << 24);
 }
 
+
 struct GatherArgs {
     const int64_t *indptr;
     const int32_t *indices;
-    const float *values;   // ratings (b weights); nullptr -> zero bias rows
-    const __half *fixed16; // (ncols, W) binary16 shadow, W = NCH * 8
-    const __half *fixed16_lo;  // split mode: binary16 residual shadow (same layout)
+    const float *values;   // ratings (b weights); nullptr -> zero bias
     int64_t nrows;
     int f;
+    int ncols;             // rows of the fixed factors; the shadow's row ncols is all zeros
+    long long *trace;      // debug timeline (CMF_TRACE builds), else unused
 };
 
-// Operand ring of NST stages + 2 TMEM accumulator hand-offs (mbarriers:
-// full[NST], empty[NST], tfull[2], tempty[2]).
-// SPLIT: every stage holds two operands, hi then lo (split-fp16 Gram,
-// D = H H^T + H L^T + L H^T), so the stage stride doubles.
-template <int NST, bool SPLIT = false>
+// Operand ring of NST stages + NBUF TMEM accumulator hand-offs (mbarriers:
+// full[NST], empty[NST], tfull[NBUF], tempty[NBUF]).
+// Stage = [hi operand 16 KB | lo operand 16 KB (SPLIT only)].
+// SPLIT: hi/lo binary16 halves of the factors (split-fp16 Gram,
+// D = H H^T + H L^T + L H^T; the ratings live in H only, so b = (H + L)^T r).
+template <int NST, bool SPLIT = false, int NBUF = 2>
 struct Pipe {
     static constexpr int kStages = NST;
-    static constexpr int kBars = 2 * NST + 4;
+    static constexpr int kBufs = NBUF;
+    static constexpr int kBars = 2 * NST + 2 * NBUF;
     static constexpr int kStageBytes = (SPLIT ? 2 : 1) * STAGE_BYTES;
     uint32_t stage_s, bar_s;
     __device__ uint32_t full(int s) const { return bar_s + 8u * s; }
     __device__ uint32_t empty(int s) const { return bar_s + 8u * (NST + s); }
     __device__ uint32_t tfull(int b) const { return bar_s + 8u * (2 * NST + b); }
-    __device__ uint32_t tempty(int b) const { return bar_s + 8u * (2 * NST + 2 + b); }
+    __device__ uint32_t tempty(int b) const { return bar_s + 8u * (2 * NST + NBUF + b); }
     __device__ uint32_t stage(int s) const { return stage_s + s * kStageBytes; }
 };
 
@@ -200,144 +202,248 @@ struct StageIter {
             if (p1 > q0) return;
         }
     }
+    __device__ void advance(int k) {
+        for (int j = 0; j < k && valid(); ++j) next();
+    }
 };
 
-// Producer warp `pw` of `nprod`: fills every stage `it` with it % nprod == pw.
-// The (index, rating) pairs of the warp's NEXT stage are loaded while the
-// current one is being gathered, so index-load latency stays off the ring.
-template <int NCH, int NST, bool SPLIT>
-__device__ void produce(const GatherArgs &g, const Pipe<NST, SPLIT> &pp, int pw, int nprod, int lane,
-                        int64_t row0, int64_t rstride) {
-    constexpr int W = NCH * 8;
-    const int pf = g.f, pf1 = g.f + 1;
-    const int pc0 = pf >> 3, pc1 = pf1 >> 3;
-    const int c = lane & 15, hrow = lane >> 4;
-    StageIter cur{0, 0, 0, g.nrows, rstride, g.indptr};
-    cur.first(row0);
-    for (int k = 0; k < pw && cur.valid(); ++k) cur.next();
-    uint32_t it = pw;
-    int idx[2] = {0, 0};
-    float rv[2] = {0.0f, 0.0f};
-    auto load_pairs = [&](const StageIter &st, int (&ix)[2], float (&r)[2]) {
+// (index, rating) of positions q0 + lane and q0 + 32 + lane of a stage; positions past
+// the row (and ids outside the shadow) read as index ncols: the shadow's zero
+// padding row.
+struct StagePairs {
+    int idx[2];
+    float val[2];
+    __device__ void load(const GatherArgs &g, const StageIter &st, int lane) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int64_t q = st.q0 + h * 32 + lane;
+            const int64_t q = st.q0 + 32 * h + lane;
             const bool ok = st.valid() && q < st.p1;
-            ix[h] = ok ? g.indices[q] : 0;
-            r[h] = (ok && g.values) ? g.values[q] : 0.0f;
+            // no use of the loaded value here: the loads stay in flight until the
+            // stage is produced (clamp_ids), two stages later
+            idx[h] = g.ncols;
+            val[h] = 0.0f;
+            if (ok) {
+                idx[h] = __ldcs(g.indices + q);
+                if (g.values) val[h] = __ldcs(g.values + q);
+            }
         }
-    };
-    load_pairs(cur, idx, rv);
-    // lanes with a plain (non-rating) chunk: 16-lane halves own rows 2t and 2t+1
-    const bool c_live = c < NCH && c != pc0 && c != pc1;
-    // swizzled destination of (row 2t + hrow, chunk c) minus its K-block part,
-    // which depends only on t & 3 (operand_addr with k = 2t + hrow)
+    }
+    // ids outside [0, ncols) gather the zero row (memory safety for bad input)
+    __device__ void clamp_ids(int ncols) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            idx[h] = static_cast<int>(min(static_cast<unsigned>(idx[h]), static_cast<unsigned>(ncols)));
+    }
+};
+
+// Debug timeline (cmf_debug_trace, compiled in only with -DCMF_TRACE): CTA 0
+// records clock64 per pipeline stage it < TRACE_STAGES: [8*it + 0] producer
+// starts waiting for the slot, +1 slot free, +2 copies issued, +3 MMA sees
+// full, +4 MMA committed; and per consumer row r < 2048 at [32768 + 4r + k].
+// The buffer pointer travels in GatherArgs::trace (kernel parameter), so a
+// stamp costs one clock read and one store.
+constexpr int TRACE_STAGES = 4096;
+static long long *g_trace_buf = nullptr;  // host side, set by cmf_debug_trace
+static inline int set_trace_buf(void *buf) {
+    g_trace_buf = static_cast<long long *>(buf);
+    return CMF_OK;
+}
+__device__ __forceinline__ void trace_at(long long *t, uint32_t idx) {
+#ifdef CMF_TRACE
+    if (t != nullptr && blockIdx.x == 0) t[idx] = clock64();
+#else
+    (void)t;
+    (void)idx;
+#endif
+}
+
+// base + ix * stride as one IMAD.WIDE.U32 (keeps the compiler from splitting
+// the 64-bit add and re-loading the base every row)
+__device__ __forceinline__ uint64_t row_addr(uint64_t base, uint32_t ix, uint32_t stride) {
+    uint64_t a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(ix), "r"(stride), "l"(base));
+    return a;
+}
+
+// Producer warp `pw` of `nprod`: fills every stage `it` with it % nprod == pw.
+// The (index, rating) pairs are loaded two of the warp's stages ahead, so the
+// index-load latency stays off the ring.  Per stage: each lane stores the
+// fp16 hi/lo ratings of positions lane, lane+32 into operand rows W, W+1 (one
+// 32-bit store each), then the warp gathers the 64 factor rows with cp.async:
+// lanes 0-15 / 16-31 take rows 2t / 2t+1, lane c%16
+// copies 16-byte chunk c of the row (a warp instruction reads two whole rows,
+// coalesced, and writes them conflict-free into the swizzled operand).  Rows
+// past the end of the CSR row up to the next 16-row K-step copy the shadow's
+// zero row; rows beyond are never read by the MMA and are skipped.  L2
+// evict_last keeps the fixed factors' shadow resident.  Completion: 32
+// cp.async.mbarrier.arrive.noinc (one per lane) + one release arrive by lane 0
+// after the rating stores, so full[s] expects 33 arrivals per stage.
+template <int NST, bool SPLIT, int NBUF>
+__device__ void produce(const GatherArgs &g, const __half *fixed16, const __half *fixed16_lo, int W,
+                        const Pipe<NST, SPLIT, NBUF> &pp, int pw, int nprod, int lane, int64_t row0,
+                        int64_t rstride) {
+    const uint64_t pol = policy_evict_last();
+    StageIter cur{0, 0, 0, g.nrows, rstride, g.indptr};
+    cur.first(row0);
+    cur.advance(pw);
+    StageIter n1 = cur;
+    n1.advance(nprod);
+    StageIter n2 = n1;
+    n2.advance(nprod);
+    StagePairs c0, c1, c2;
+    c0.load(g, cur, lane);
+    c1.load(g, n1, lane);
+    c2.load(g, n2, lane);
+    const int c = lane & 15, hrow = lane >> 4;
+    const bool live = c < (W >> 3);
+    const uint32_t W2 = static_cast<uint32_t>(W) * 2;
+    const uint64_t src_hi = reinterpret_cast<uint64_t>(fixed16) + c * 16;
+    const uint64_t src_lo = reinterpret_cast<uint64_t>(fixed16_lo) + c * 16;
+    // swizzled destination of (row 2t + hrow, chunk c): depends on t only via
+    // t & 3 (row within the 8-row atom) and t >> 2 (K-block, +1024 B)
     uint32_t dst_off[4];
 #pragma unroll
     for (int t4 = 0; t4 < 4; ++t4) dst_off[t4] = operand_addr(0, 2 * t4 + hrow, c);
+    // rating slots: operand row k, chunk W/8 (halves 0, 1 = features W, W+1)
+    uint32_t r_off[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) r_off[h] = operand_addr(0, 32 * h + lane, W >> 3);
+    uint32_t it = pw;
     while (cur.valid()) {
-        StageIter nxt = cur;
-        for (int k = 0; k < nprod && nxt.valid(); ++k) nxt.next();
-        int idx_n[2];
-        float rv_n[2];
-        load_pairs(nxt, idx_n, rv_n);
-        const int64_t q0 = cur.q0, p1 = cur.p1;
         const int s = it % NST;
-        // rating chunk(s) of rows lane, lane+32: loads issued before the wait
-        uint4 pv[2][2];
+        const int nrem16 = static_cast<int>(min(static_cast<int64_t>(KS), cur.p1 - cur.q0) + 15) & ~15;
+        c0.clamp_ids(g.ncols);
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 0);
+        mbar_wait_backoff(pp.empty(s), ((it / NST) & 1) ^ 1);
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 1);
+        const uint32_t stg = pp.stage(s);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const bool ok = q0 + h * 32 + lane < p1;
-            const __half *row = g.fixed16 + static_cast<int64_t>(idx[h]) * W;
-            pv[h][0] = ok ? __ldg(reinterpret_cast<const uint4 *>(row + 8 * pc0)) : make_uint4(0, 0, 0, 0);
-            pv[h][1] = (ok && pc1 != pc0) ? __ldg(reinterpret_cast<const uint4 *>(row + 8 * pc1))
-                                          : make_uint4(0, 0, 0, 0);
+            const __half hi = __float2half_rn(c0.val[h]);
+            const __half lo = __float2half_rn(c0.val[h] - __half2float(hi));
+            const uint32_t v = static_cast<uint32_t>(__half_as_ushort(hi)) |
+                               (static_cast<uint32_t>(__half_as_ushort(lo)) << 16);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + r_off[h]), "r"(v) : "memory");
         }
-        mbar_wait_backoff(pp.empty(s), ((it / NST) & 1) ^ 1);
-        const uint32_t stg = pp.stage(s);
-        const int nrem = static_cast<int>(min(static_cast<int64_t>(KS), p1 - q0));
+        fence_proxy_async();  // generic-proxy rating stores -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pp.full(s));  // release: the rating stores
 #pragma unroll
         for (int t = 0; t < KS / 2; ++t) {
-            const int k = 2 * t + hrow;
-            // every lane holds (index) pairs for rows lane and lane + 32: full-warp shuffle
-            const int ix = __shfl_sync(0xffffffffu, t < 16 ? idx[0] : idx[1], k & 31);
-            const bool valid = k < nrem;
-            const int64_t off = static_cast<int64_t>(ix) * W + 8 * c;
-            const __half *src = valid ? g.fixed16 + off : g.fixed16;
+            if ((t & 7) == 0 && 2 * t >= nrem16) break;  // whole K-steps only (warp-uniform)
+            // row 2t + hrow: position (2t + hrow) & 31 of register half t >> 4
+            const uint32_t ix = static_cast<uint32_t>(__shfl_sync(0xffffffffu, c0.idx[t >> 4], (2 * t + hrow) & 31));
             const uint32_t dst = stg + dst_off[t & 3] + (t >> 2) * KBLK_BYTES;
-            if (c_live) cp_async16_zfill(dst, src, valid ? 16u : 0u);
-            if (SPLIT && c < NCH)  // residual operand: every chunk (its rating slots stay zero)
-                cp_async16_zfill(dst + STAGE_BYTES, valid ? g.fixed16_lo + off : g.fixed16_lo, valid ? 16u : 0u);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int k = h * 32 + lane;
-            const bool ok = q0 + k < p1;
-            const __half hi = __float2half_rn(rv[h]);
-            const __half lo = __float2half_rn(rv[h] - __half2float(hi));
-            uint4 v0 = pv[h][0], v1 = pv[h][1];
-            if (ok) {
-                set_half(v0, pf & 7, __half_as_ushort(hi));
-                if (pc1 == pc0) set_half(v0, pf1 & 7, __half_as_ushort(lo));
-                else set_half(v1, pf1 & 7, __half_as_ushort(lo));
-            }
-            const uint32_t d0 = operand_addr(stg, k, pc0);
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d0), "r"(v0.x), "r"(v0.y), "r"(v0.z),
-                         "r"(v0.w)
-                         : "memory");
-            if (pc1 != pc0) {
-                const uint32_t d1 = operand_addr(stg, k, pc1);
-                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d1), "r"(v1.x), "r"(v1.y), "r"(v1.z),
-                             "r"(v1.w)
+            if (live) {
+                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst),
+                             "l"(row_addr(src_hi, ix, W2)), "l"(pol)
                              : "memory");
+                if (SPLIT)
+                    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                                     dst + STAGE_BYTES),
+                                 "l"(row_addr(src_lo, ix, W2)), "l"(pol)
+                                 : "memory");
             }
         }
-        fence_proxy_async();
-        cp_async_arrive_noinc(pp.full(s));
-        cur = nxt;
-        idx[0] = idx_n[0];
-        idx[1] = idx_n[1];
-        rv[0] = rv_n[0];
-        rv[1] = rv_n[1];
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(pp.full(s)) : "memory");
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 2);
+        cur = n1;
+        n1 = n2;
+        n2.advance(nprod);
+        c0 = c1;
+        c1 = c2;
+        c2.load(g, n2, lane);
         it += nprod;
     }
 }
 
-// Single-thread MMA issuer: one accumulator chain per non-empty row into TMEM
-// buffer (row counter & 1); releases stages with tcgen05.commit.
-template <int NST, bool SPLIT>
-__device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, SPLIT> &pp, uint32_t tmem_base,
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred;
+}
+
+// MMA issuer, run by a whole warp (warp-uniform control flow keeps the
+// descriptors in uniform registers; one elected lane issues): one accumulator
+// chain per non-empty row into TMEM buffer (row counter % NBUF), one 128 x N
+// MMA per 16-row K-step; releases stages with tcgen05.commit.  Buffer b
+// occupies columns [b*N, (b+1)*N).  The next row's extent is loaded one row
+// ahead so the indptr latency stays off the issue loop.
+template <int NST, bool SPLIT, int NBUF>
+__device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, SPLIT, NBUF> &pp, uint32_t tmem_base,
                                           int N, int64_t row0, int64_t rstride) {
     const uint32_t idesc = make_idesc(M, N);
+    const uint64_t desc0 = make_desc(pp.stage(0));
+    // descriptor start address field is (addr >> 4): stage s, K-step kk adds
+    // (s * kStageBytes + kk * 2048) >> 4; the lo operand adds STAGE_BYTES >> 4
+    constexpr uint32_t kStageStep = Pipe<NST, SPLIT, NBUF>::kStageBytes >> 4;
+    constexpr uint32_t kKStep = (2 * KBLK_BYTES) >> 4;
+    constexpr uint32_t kLoStep = STAGE_BYTES >> 4;
     uint32_t it = 0, rowc = 0;
-    for (int64_t u = row0; u < g.nrows; u += rstride) {
-        const int64_t p0 = g.indptr[u], p1 = g.indptr[u + 1];
-        if (p1 == p0) continue;
-        const int b = rowc & 1;
-        mbar_wait(pp.tempty(b), ((rowc >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + b * 128;
-        uint32_t acc = 0;
-        for (int64_t q0 = p0; q0 < p1; q0 += KS, ++it) {
-            const int s = it % NST;
-            mbar_wait(pp.full(s), (it / NST) & 1);
+    int64_t u = row0;
+    int64_t p0 = u < g.nrows ? g.indptr[u] : 0, p1 = u < g.nrows ? g.indptr[u + 1] : 0;
+    while (u < g.nrows) {
+        const int64_t un = u + rstride;
+        const int64_t q0n = un < g.nrows ? g.indptr[un] : 0, q1n = un < g.nrows ? g.indptr[un + 1] : 0;
+        if (p1 > p0) {
+            const int b = rowc % NBUF;
+            mbar_wait(pp.tempty(b), ((rowc / NBUF) & 1) ^ 1);
             tc_fence_after();
-            const int nb = static_cast<int>(min(static_cast<int64_t>(KS), p1 - q0));
-            const uint32_t sbase = pp.stage(s);
-            for (int kk = 0; kk < (nb + 15) / 16; ++kk) {
-                const uint64_t d = make_desc(sbase + kk * 2 * KBLK_BYTES);
-                tc_mma(tmem_d, d, d, idesc, acc);
-                acc = 1;
-                if (SPLIT) {  // + H L^T + L H^T into the same accumulator
-                    const uint64_t dl = make_desc(sbase + STAGE_BYTES + kk * 2 * KBLK_BYTES);
-                    tc_mma(tmem_d, d, dl, idesc, 1);
-                    tc_mma(tmem_d, dl, d, idesc, 1);
+            const uint32_t tmem_d = tmem_base + b * N;
+            uint32_t acc = 0;
+            for (int64_t q0 = p0; q0 < p1; q0 += KS, ++it) {
+                const int s = it % NST;
+                mbar_wait(pp.full(s), (it / NST) & 1);
+                if (lane_id() == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 3);
+                tc_fence_after();
+                const int nk = static_cast<int>(min(static_cast<int64_t>(KS), p1 - q0) + 15) >> 4;
+                const uint64_t ds = desc0 + s * kStageStep;
+                if (elect_one()) {
+                    for (int kk = 0; kk < nk; ++kk) {
+                        const uint64_t d = ds + kk * kKStep;
+                        tc_mma(tmem_d, d, d, idesc, acc | kk);
+                        if (SPLIT) {  // + H L^T + L H^T
+                            tc_mma(tmem_d, d, d + kLoStep, idesc, 1);
+                            tc_mma(tmem_d, d + kLoStep, d, idesc, 1);
+                        }
+                    }
+                    tc_commit(pp.empty(s));
                 }
+                __syncwarp();
+                acc = 1;
+                if (lane_id() == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 4);
             }
-            tc_commit(pp.empty(s));
+            if (elect_one()) tc_commit(pp.tfull(b));
+            __syncwarp();
+            ++rowc;
         }
-        tc_commit(pp.tfull(b));
-        ++rowc;
+        u = un;
+        p0 = q0n;
+        p1 = q1n;
+    }
+}
+
+// Zero-initialise the operand ring (chunks past the rating slots are never
+// written again) and the barriers; call from all threads, then sync.
+template <int NST, bool SPLIT, int NBUF>
+__device__ void pipe_init(const Pipe<NST, SPLIT, NBUF> &pp, unsigned char *stage_mem, int nthreads,
+                          uint32_t full_count, uint32_t tempty_count) {
+    for (int i = threadIdx.x; i < NST * Pipe<NST, SPLIT, NBUF>::kStageBytes / 16; i += nthreads)
+        reinterpret_cast<int4 *>(stage_mem)[i] = make_int4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(pp.full(s), full_count);
+            mbar_init(pp.empty(s), 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(pp.tfull(b), 1);
+            mbar_init(pp.tempty(b), tempty_count);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 }
 

@@ -204,7 +204,8 @@ def assemble_side(view: RowView, theta, lam: float, cfg: TileConfig | None = Non
         stride = (P + 7) // 8 * 8  # 16-byte rows
         a_full = torch.empty((nrows, stride), dtype=dt, device=dev)
         w16 = nat.tc_width(f)
-        shadow = torch.empty((2 if split else 1, th.shape[0], w16), dtype=torch.float16, device=dev)
+        # (+1 row: the all-zero row the gather reads for padding positions)
+        shadow = torch.empty((2 if split else 1, th.shape[0] + 1, w16), dtype=torch.float16, device=dev)
         scale = 64.0
         if split:
             nat.call("cmf_factors_to_half_split", nat.ptr(th), th.shape[0], f, nat.ptr(shadow[0]),
@@ -213,7 +214,7 @@ def assemble_side(view: RowView, theta, lam: float, cfg: TileConfig | None = Non
             nat.call("cmf_factors_to_half", nat.ptr(th), th.shape[0], f, nat.ptr(shadow[0]), w16,
                      nat.stream_ptr())
         nat.call("cmf_gram_assemble_tc", nat.ptr(indptr), nat.ptr(indices), nat.ptr(bw), nrows,
-                 nat.ptr(shadow[0]), nat.ptr(shadow[1]) if split else None, scale, w16, f,
+                 nat.ptr(shadow[0]), nat.ptr(shadow[1]) if split else None, th.shape[0], scale, w16, f,
                  float(lam), int(bool(weighted_reg)), nat.ptr(base),
                  nat.PREC[precision], nat.ptr(a_full), stride, nat.ptr(b_out), nat.ptr(nu),
                  nat.ptr(flag), nat.stream_ptr())

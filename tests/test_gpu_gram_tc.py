@@ -49,7 +49,8 @@ def _f64_reference(view, theta, lam, weighted=True):
     (8, [3, 40, 0]),
     (1, [5, 0, 9]),
     (63, [100, 2000, 64]),
-    (126, [129, 7]),
+    (120, [129, 7]),
+    (112, [65, 3]),
 ])
 @pytest.mark.parametrize("precision", ["fp16", "fp32"])
 def test_tc_gram_matches_fp16_operand_reference(cuda_device, f, degs, precision):
@@ -76,7 +77,7 @@ def test_tc_gram_close_to_reference_fp32(golden, cuda_device):
     for ci in range(int(g["ncases"])):
         p = f"c{ci}_"
         m, n, f = (int(v) for v in g[p + "meta"])
-        if f > 126:
+        if f > 120:
             continue
         view = RowView(g[p + "row_ptr"], g[p + "col_idx"], g[p + "csr_val"], m, n)
         theta = g[p + "theta_n"]
@@ -132,7 +133,7 @@ def test_split_precision_gram_is_fp32_faithful(golden, oracle, cuda_device):
     for ci in range(int(g["ncases"])):
         p = f"c{ci}_"
         m, n, f = (int(v) for v in g[p + "meta"])
-        if f > 126:
+        if f > 120:
             continue
         for side in ("x", "t"):
             if side == "x":

@@ -1,0 +1,59 @@
+"""Pipeline timeline of CTA 0 of the fused kernel (cmf_debug_trace) at Netflix shape.
+
+python tools/trace_fused.py [--side t|x] -> per-stage latencies (cycles)."""
+import argparse, os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_1808_03843_b200 as cmfb
+from paper_1808_03843_b200 import _native as nat
+from paper_1808_03843_b200.als import HalfUpdatePlan
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--side", default="t")
+ap.add_argument("--kernel", default="tc")
+a = ap.parse_args()
+m, n, nnz, f = 480_189, 17_770, 99_000_000, 100
+train, test = cmfb.gen_synthetic_device(m, n, f, nnz, 0.1, 0.1, seed=0)
+x = torch.from_numpy(cmfb.init_factors(m, f, 0.1, [0, 0])).cuda()
+th = torch.from_numpy(cmfb.init_factors(n, f, 0.1, [0, 1])).cuda()
+view, fixed, target = (train.csc_view(), x, th) if a.side == "t" else (train.csr_view(), th, x)
+solver = cmfb.SolverConfig("cg", precision="fp16")
+plan = HalfUpdatePlan(view.nrows, f, solver, x.device)
+plan.launch(view.indptr, view.indices, view.values, fixed, target.clone(), 0.05, True, a.kernel)
+buf = torch.zeros(8 * 4096 + 4 * 2048 + 64 * 64, dtype=torch.int64, device="cuda")
+nat.call("cmf_debug_trace", nat.ptr(buf))
+plan.launch(view.indptr, view.indices, view.values, fixed, target.clone(), 0.05, True, a.kernel)
+torch.cuda.synchronize()
+nat.call("cmf_debug_trace", None)
+allb = buf.cpu().numpy()
+ev = allb[40960:40960 + 4096].reshape(64, 64).astype(np.float64)
+for r in (3, 30, 60):
+    e = ev[r][ev[r] > 0]
+    if len(e) > 2:
+        print("row", r, "CG events (cycles from first):", (e - e[0]).astype(int).tolist())
+rr = allb[32768:40960].reshape(2048, 4).astype(np.float64)
+rr = rr[(rr[:, 3] > 0) & (rr[:, 0] > 0)]
+if len(rr) > 8:
+    mid = rr[len(rr) // 4: 3 * len(rr) // 4]
+    print("CG rows traced", len(rr))
+    print("CG wait for accumulator (1-0): %.0f" % np.median(mid[:, 1] - mid[:, 0]))
+    print("CG TMEM load + release  (2-1): %.0f" % np.median(mid[:, 2] - mid[:, 1]))
+    print("CG solve                (3-2): %.0f" % np.median(mid[:, 3] - mid[:, 2]))
+t = allb[:32768].reshape(4096, 8)[:, :5].astype(np.float64)
+ok = (t[:, 4] > 0) & (t[:, 0] > 0)
+t = t[ok]
+t -= t[0, 0]
+k = len(t)
+print("stages traced", k)
+lo, hi = k // 4, 3 * k // 4
+mid = t[lo:hi]
+print("per-stage interval (MMA commit to commit): %.0f cyc" % np.median(np.diff(mid[:, 4])))
+print("producer slot wait      (1-0): %.0f" % np.median(mid[:, 1] - mid[:, 0]))
+print("producer issue          (2-1): %.0f" % np.median(mid[:, 2] - mid[:, 1]))
+print("data latency to MMA     (3-2): %.0f  p90 %.0f" % (np.median(mid[:, 3] - mid[:, 2]), np.percentile(mid[:, 3] - mid[:, 2], 90)))
+print("MMA issue               (4-3): %.0f" % np.median(mid[:, 4] - mid[:, 3]))
+print("slot free -> MMA sees   (3-1): %.0f" % np.median(mid[:, 3] - mid[:, 1]))
+for i in range(lo, lo + 12):
+    print(i, (t[i] - t[lo, 0]).astype(int).tolist())
