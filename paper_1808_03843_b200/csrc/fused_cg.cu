@@ -39,6 +39,8 @@ namespace tc {
 
 constexpr int F_PROD = 7;  // producer warps: the gather rate scales with issuing warps
 constexpr int CG_THREADS = 128;
+constexpr int MVB_OPERAND = 4096;  // matvec B operand: 16 rows x 128 halves, K-major SW128 (2 K-atoms)
+constexpr int MVB_BYTES = 5120;    // + warp partials, 1024-aligned per group
 // NG CG groups (== TMEM accumulator buffers, one warpgroup each) + 2 auxiliary
 // warpgroups (7 producers + the MMA warp).  Registers are rebalanced with
 // setmaxnreg: the CG warpgroups hold a register row of A_u (4*FC floats) and
@@ -69,6 +71,7 @@ struct FusedArgs {
     GatherArgs gather;
     const __half *fixed16;  // binary16 shadow of the fixed factors (ncols, W)
     int W, N, tmem_cols;  // shadow width, accumulator width (Gram + rating columns W, W+1)
+    int dmv_tail, dmv_off;  // matvec result columns: after the NBUF buffers, or inside each buffer
     double lam;
     int weighted;
     float *target;  // (nrows, f) in/out
@@ -141,6 +144,37 @@ __device__ __forceinline__ void tmem_load_row(uint32_t taddr, uint32_t (&v)[NC])
     tmem_ld_wait();
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t *v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]: kind::f16, A operand read from tensor memory
+__device__ __forceinline__ void tc_mma_tmem_a(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// K-major, 128-byte swizzle (8 rows x 128 B atoms, SBO = 1024 B between 8-row
+// groups); a K-step adds its byte offset to the start address.
+__device__ __forceinline__ uint64_t make_desc_kmajor(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>((1024 >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     uint32_t v;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
@@ -155,25 +189,29 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
     constexpr int F_MMA_WARP = FusedShape<FC>::MMA_WARP;
     constexpr int NBUF = FusedShape<FC>::NBUF;
     using PipeT = FPipe<NBUF>;
-    constexpr int NC = FC * 4;                 // matvec columns (>= f)
-    constexpr int NFULL = NC / 32, REM = NC % 32;
-    constexpr int NPAD = (NC + 31) / 32 * 32;  // p-vector buffer (zero past f)
-    static_assert(REM % 4 == 0, "tail chunk must be a multiple of 4 columns");
+    constexpr int KP = (FC * 4 + 15) / 16 * 16;  // matvec K extent (>= f), 16-half MMA steps
+    constexpr int NKS = KP / 16;                  // kind::f16 MMAs per matvec
     constexpr int F_STAGES = PipeT::kStages;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const GatherArgs &ga = g.gather;
     const int f = ga.f;
     unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    // [stages | per-group CG scratch: p (FC*4 floats) x2 buffers, red 2 x 12 floats | barriers | tmem slot]
-    float *scratch = reinterpret_cast<float *>(smem + F_STAGES * PipeT::kStageBytes);
-    constexpr int SCR = 2 * ((FC * 4 + 31) / 32 * 32) + 32;  // floats per group: vector x2, red 2 x 8 (+pad)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(scratch + F_GROUPS * SCR);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + PipeT::kBars);
+    // [stages | per-group CG scratch (MVB_BYTES each: matvec B operand, warp partials) |
+    //  barriers (pipeline + one matvec barrier per group) | tmem slot]
+    unsigned char *scratch = smem + F_STAGES * PipeT::kStageBytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(scratch + F_GROUPS * MVB_BYTES);
+    uint64_t *mvbars = bars + PipeT::kBars;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mvbars + F_GROUPS);
     PipeT pp{smem_u32(smem), smem_u32(bars)};
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     pipe_init(pp, smem, F_THREADS, 33, CG_THREADS);
-    for (int i = tid; i < F_GROUPS * SCR; i += F_THREADS) scratch[i] = 0.0f;
+    for (int i = tid; i < F_GROUPS * MVB_BYTES / 16; i += F_THREADS)
+        reinterpret_cast<int4 *>(scratch)[i] = make_int4(0, 0, 0, 0);
+    if (tid == 0) {
+        for (int q = 0; q < F_GROUPS; ++q) mbar_init(smem_u32(mvbars + q), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (warp == F_MMA_WARP) tmem_alloc(smem_u32(tmem_slot), g.tmem_cols);
     fence_proxy_async();
     tc_fence_before();
@@ -208,12 +246,21 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
         const int grp = warp >> 2;             // rows r with r % NG == grp
         const int i = (warp & 3) * 32 + lane;  // row of A_u == TMEM lane
         const int bar_id = 1 + grp;
-        float *pvec = scratch + grp * SCR;     // 2 x NPAD floats (double buffer), zero past f
-        float *red = pvec + 2 * NPAD;          // 2 x 8 floats: warp partials of two dot products
+        unsigned char *mine_s = scratch + grp * MVB_BYTES;
+        const uint32_t bop = smem_u32(mine_s);               // matvec B operand (K-major SW128)
+        float *red = reinterpret_cast<float *>(mine_s + MVB_OPERAND);  // 2 x 8 warp partials
+        const uint32_t mvbar = smem_u32(mvbars + grp);
+        // B(n, k): n = 0 / 1 hold the vector's fp16 hi / lo halves at K position k = i
+        const uint32_t bofs0 = (i / 64) * 2048 + ((((i % 64) >> 3) ^ 0) << 4) + (i & 7) * 2;
+        const uint32_t bofs1 = (i / 64) * 2048 + 128 + ((((i % 64) >> 3) ^ 1) << 4) + (i & 7) * 2;
         const bool act = i < f;
+        const bool leader = (warp & 3) == 0;  // issues the group's matvec MMAs
+        constexpr uint32_t idesc_mv = (1u << 4) | (static_cast<uint32_t>(16 >> 3) << 17) |
+                                      (static_cast<uint32_t>(128 >> 4) << 24);  // f16 x f16 -> f32, K-major
         int32_t brk = 0;
-        uint32_t rowc = 0;         // non-empty rows of this CTA so far (all groups)
-        int slot = 0, pb = 0;      // reduction / p-vector buffers alternate across rows too
+        uint32_t rowc = 0;    // non-empty rows of this CTA so far (all groups)
+        uint32_t mvph = 0;    // matvec barrier phase
+        int slot = 0;         // reduction buffers alternate
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
             const int64_t p0 = ga.indptr[u];
@@ -222,41 +269,64 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
             const uint32_t r_here = rowc++;
             if (r_here % F_GROUPS != static_cast<uint32_t>(grp)) continue;
             const int b = r_here % NBUF;
+            float* const tgt = g.target + u * f;
+            float xi = act ? tgt[i] : 0.0f;  // warm start, loaded while the Gram is built
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 0);
             mbar_wait_backoff(pp.tfull(b), (r_here / NBUF) & 1);  // sleeps: long rows keep the group idle
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 1);
             tc_fence_after();
-            // A_u stays in TMEM for the whole solve (thread i <-> lane i <-> row i):
-            // every matvec streams the row in 16-column chunks, double-buffered.
-            // Columns [f, NPAD) meet zero p entries; rows >= f are zero padding
-            // except the two rating rows W, W+1, so threads i >= f zero their y.
+            // A_u (fp32, thread i <-> lane i <-> row i) -> binary16 in place: columns
+            // [32c, 32c+32) become packed columns [16c, 16c+16), the tcgen05 A-operand
+            // layout (lane = row, column j = elements 2j, 2j+1).  RNE, as the
+            // reference's fp16 Hermitian storage.  Rows >= f (padding and the two
+            // rating rows) become zero; the bias columns W, W+1 are read first.
             const uint32_t tb = tmem_base + lane_base + b * g.N;
             float bi = __uint_as_float(tmem_ld1(tb + g.W)) + __uint_as_float(tmem_ld1(tb + g.W + 1));
             tmem_ld_wait();
             bi = act ? bi : 0.0f;
+#pragma unroll
+            for (int c = 0; c < (KP + 31) / 32; ++c) {
+                uint32_t v[32];
+                tmem_ldn<32>(tb + 32 * c, v);
+                tmem_ld_wait();
+                uint32_t h[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const __half2 hv = __floats2half2_rn(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                    h[j] = act ? *reinterpret_cast<const uint32_t *>(&hv) : 0u;
+                }
+                tmem_st16(tb + 16 * c, h);
+            }
+            tmem_st_wait();
+            tc_fence_before();
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 2);
-            int ev = 0;
+            const uint32_t dcol = g.dmv_tail ? tmem_base + NBUF * g.N + 16 * grp
+                                             : tmem_base + b * g.N + g.dmv_off;
+            const uint32_t a_tmem = tmem_base + b * g.N;
             const float reg = g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
                                          : __double2float_rn(g.lam);
             // One barrier per exchange: thread i publishes its entry of the vector
-            // to multiply and the warp sums of two dot products, then every thread
-            // reads the vector and the 4 warp partials.  The first 32-column chunk
-            // of the A row is requested from TMEM before the barrier.
+            // (fp16 hi/lo into the B operand) and the warp sums of two dot
+            // products; after the barrier one thread issues the matvec on the
+            // tensor core (A from TMEM) while every thread finishes the sums.
             //   y_i = (A_u v)_i + reg * v_i,  (sa, sb) = group sums of (da, db)
+            int ev = 0;
             auto exchange = [&](float v, float da, float db, float &sa, float &sb, bool mv) -> float {
-                uint32_t abuf[2][32];
                 if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
-                if (mv) tmem_ldn<32>(tb, abuf[0]);
+                if (mv && act) {
+                    const __half hv = __float2half_rn(v);
+                    const __half lv = __float2half_rn(v - __half2float(hv));
+                    asm volatile("st.shared.b16 [%0], %1;" ::"r"(bop + bofs0), "h"(__half_as_ushort(hv)) : "memory");
+                    asm volatile("st.shared.b16 [%0], %1;" ::"r"(bop + bofs1), "h"(__half_as_ushort(lv)) : "memory");
+                }
+                if (mv) fence_proxy_async();
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     da += __shfl_xor_sync(0xffffffffu, da, o);
                     db += __shfl_xor_sync(0xffffffffu, db, o);
                 }
-                float *pv = pvec + pb * NPAD;
                 float *rd = red + 8 * slot;
-                pb ^= 1;
                 slot ^= 1;
-                if (act) pv[i] = v;
                 if (lane == 0) {
                     rd[warp & 3] = da;
                     rd[4 + (warp & 3)] = db;
@@ -264,35 +334,28 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
                 if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
                 named_bar(bar_id, CG_THREADS);
                 if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
+                if (mv && leader) {
+                    if (elect_one()) {
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < NKS; ++kk)
+                            tc_mma_tmem_a(dcol, a_tmem + 8 * kk,
+                                          make_desc_kmajor(bop + (kk >> 2) * 2048 + (kk & 3) * 32), idesc_mv, kk);
+                        tc_commit(mvbar);
+                    }
+                    __syncwarp();
+                }
                 sa = (rd[0] + rd[1]) + (rd[2] + rd[3]);
                 sb = (rd[4] + rd[5]) + (rd[6] + rd[7]);
                 if (!mv) return 0.0f;
-                const float4 *p4 = reinterpret_cast<const float4 *>(pv);
-                float2 ya = make_float2(0.0f, 0.0f), yb = make_float2(0.0f, 0.0f);
-                auto chunk = [&](const uint32_t *av, int c0, int ncol) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        if (4 * q < ncol) {
-                            const float4 pq = p4[c0 / 4 + q];
-                            ya = __ffma2_rn(make_float2(__uint_as_float(av[4 * q]), __uint_as_float(av[4 * q + 1])),
-                                            make_float2(pq.x, pq.y), ya);
-                            yb = __ffma2_rn(make_float2(__uint_as_float(av[4 * q + 2]), __uint_as_float(av[4 * q + 3])),
-                                            make_float2(pq.z, pq.w), yb);
-                        }
-                    }
-                };
-#pragma unroll
-                for (int c = 0; c < NFULL; ++c) {
-                    tmem_ld_wait();  // chunk c has landed
-                    if (c + 1 < NFULL) tmem_ldn<32>(tb + 32 * (c + 1), abuf[(c + 1) & 1]);
-                    else if (REM) tmem_ld_tail<REM>(tb + 32 * NFULL, abuf[(c + 1) & 1]);
-                    chunk(abuf[c & 1], 32 * c, 32);
-                }
-                if (REM) {
-                    tmem_ld_wait();
-                    chunk(abuf[NFULL & 1], 32 * NFULL, REM);
-                }
-                const float y = act ? (ya.x + ya.y) + (yb.x + yb.y) : 0.0f;
+                mbar_wait(mvbar, mvph & 1);
+                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
+                ++mvph;
+                tc_fence_after();
+                const float y0 = __uint_as_float(tmem_ld1(dcol + lane_base));
+                const float y1 = __uint_as_float(tmem_ld1(dcol + lane_base + 1));
+                tmem_ld_wait();
+                const float y = act ? y0 + y1 : 0.0f;
                 if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
                 return fmaf(reg, v, y);
             };
@@ -301,8 +364,6 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
             // recurrences, so each iteration needs ONE exchange: (r.r, w.r) and
             // m = A w together.  Semantics as the reference: at least one update
             // unless p^T A p <= 0 (breakdown, x kept); stop once ||r|| < eps.
-            float* const tgt = g.target + u * f;
-            float xi = act ? tgt[i] : 0.0f;
             float bb, unused;
             float r = bi - exchange(xi, bi * bi, 0.0f, bb, unused, true);
             const float eps2 = g.tol * g.tol * bb;
@@ -355,10 +416,15 @@ template <int FC>
 static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
     using Shape = tc::FusedShape<FC>;
     using PipeT = tc::FPipe<Shape::NBUF>;
-    constexpr int SCR = 2 * ((FC * 4 + 31) / 32 * 32) + 32;
-    const size_t smem = 1024 + PipeT::kStages * PipeT::kStageBytes + Shape::NG * SCR * sizeof(float) +
-                        PipeT::kBars * 8 + 16;
-    g.tmem_cols = Shape::NBUF * g.N <= 256 ? 256 : 512;
+    const size_t smem = 1024 + PipeT::kStages * PipeT::kStageBytes + Shape::NG * tc::MVB_BYTES +
+                        (PipeT::kBars + Shape::NG) * 8 + 16;
+    // matvec results (16 columns per group): after the accumulators when they fit,
+    // else in each buffer's columns freed by the fp16 repacking of A_u
+    constexpr int KP = (FC * 4 + 15) / 16 * 16;
+    g.dmv_tail = Shape::NBUF * g.N + 16 * Shape::NG <= 512;
+    g.dmv_off = (KP / 2 + 15) / 16 * 16;
+    if (!g.dmv_tail && g.dmv_off + 16 > g.N) return set_error(CMF_EINVAL, "fused CG: no TMEM room for f=%d", g.gather.f);
+    g.tmem_cols = 512;
     auto k = tc::fused_cg_kernel<FC>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return set_error(CMF_ECUDA, "fused_cg smem attr: %s", cudaGetErrorString(e));
