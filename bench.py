@@ -46,7 +46,7 @@ SOLVERS = {"cg16": ("cg", "fp16"), "cg32": ("cg", "fp32"), "exact": ("exact", "f
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shape", default="netflix", choices=list(SHAPES))
@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -318,9 +318,10 @@ def main():
     tt = traffic_table()
     dominant = max((fused_ms, "fused"), (gram_ms, "gram"), (solve_ms, "solve"))[1]
     if dominant == "fused":
-        roof = {"kernel": "fused_cg_kernel (K1 tcgen05 Gram + K3 CG in TMEM/registers)",
+        roof = {"kernel": "fused_cg_kernel (K1 tcgen05 Gram + K3 CG, A_u never leaves TMEM)",
                 "bound": "tensor", "achieved": fused_tflops, "peak": pk["tensor"], "unit": "TFLOP/s",
-                "traffic": tt.get("fused")}
+                "traffic": tt.get("fused_cg_kernel", {}).get("bytes_per_step"),
+                "traffic_note": tt.get("fused_cg_kernel", {}).get("note")}
     elif dominant == "gram":
         if gram_kernel.startswith("tc"):
             roof = {"kernel": "gram_tc_kernel (K1)", "bound": "tensor", "achieved": gram_tflops,

@@ -30,9 +30,9 @@ def launches(path):
         name = r["Kernel Name"].split("(")[0]
         v = float(r["Metric Value"])
         unit = r.get("Metric Unit", "")
-        if unit == "nsecond":
+        if unit in ("nsecond", "ns"):
             v /= 1e3
-        elif unit == "msecond":
+        elif unit in ("msecond", "ms"):
             v *= 1e3
         per.setdefault(name, []).append(v)
     total = sum(sum(v) for v in per.values())
