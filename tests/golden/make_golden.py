@@ -18,6 +18,10 @@ Fixtures:
   data_cases.npz    gen_synthetic / split_holdout / init_factors draws
   train_small.npz   full train() trajectories (X, Theta per epoch) on a small
                     instance for exact / cg-fp32 / cg-fp16
+  implicit_small.npz  implicit_train (reference implicit.py) on a small
+                    non-negative instance: X, Theta, objectives and preference
+                    RMSE per epoch (exact, cg-fp32), one
+                    implicit_update_side and precompute_gram, mean percentile rank
   train_ml1m.npz    MovieLens-1M-shaped protocol (BASELINE configs[0]): RMSE and
                     objective per epoch for exact / cg-fp32 / cg-fp16, sampled
                     factor rows per epoch (exact), and SHA-256 digests of the
@@ -275,11 +279,61 @@ def train_ml1m(cmf):
     np.savez_compressed(os.path.join(OUT, "train_ml1m.npz"), **out)
 
 
+def implicit_small(cmf):
+    import cmf.implicit as imp
+    out = {}
+    m, n, nnz, f = 300, 160, 4000, 12
+    rng = np.random.default_rng(11)
+    flat = np.sort(rng.choice(m * n, size=nnz, replace=False))
+    vals = rng.integers(1, 6, size=nnz).astype(np.float32)  # play counts / stars
+    t = cmf.Triples((flat // n).astype(np.int64), (flat % n).astype(np.int64), vals)
+    tr, te = cmf.split_holdout(t, 0.1, 3)
+    sr = cmf.build(tr, m + 2, n)  # two users without observations
+    out["meta"] = np.array([m + 2, n, f], np.int64)
+    for name, a in (("row_ptr", sr.row_ptr), ("col_idx", sr.col_idx), ("csr_val", sr.csr_val),
+                    ("col_ptr", sr.col_ptr), ("row_idx", sr.row_idx), ("csc_val", sr.csc_val)):
+        out[name] = a
+    out["te_u"], out["te_v"], out["te_r"] = te.user, te.item, te.rating
+    theta = cmf.init_factors(n, f, 0.1, [0, 1])
+    x0 = cmf.init_factors(m + 2, f, 0.1, [0, 0])
+    g = imp.precompute_gram(theta)
+    out["gram_theta"] = g
+    x1 = x0.copy()
+    imp.implicit_update_side(sr.csr_view(), theta, g, x1, 40.0, 0.05, cmf.SolverConfig("exact"))
+    out["x0"], out["x1_exact"] = x0, x1
+    for name, cfg in (("exact", cmf.SolverConfig("exact")),
+                      ("cg32", cmf.SolverConfig("cg", 6, 1e-4, "fp32"))):
+        # (fp16 storage overflows binary16 here: alpha r F^T F exceeds 65504 -- the
+        # reference raises NumericalError, and so does the B200 path)
+        xs, ts = [], []
+        orig = imp.implicit_update_side
+
+        def spy(view, fixed, gram, target, *a, **k):
+            r = orig(view, fixed, gram, target, *a, **k)
+            (xs if target.shape[0] == m + 2 else ts).append(target.copy())
+            return r
+        imp.implicit_update_side = spy
+        try:
+            X, T, rep = imp.implicit_train(sr, imp.ImplicitConfig(f=f, alpha=40.0, lam=0.05, epochs=4,
+                                                                  solver=cfg), te)
+        finally:
+            imp.implicit_update_side = orig
+        out[name + "_X"], out[name + "_T"] = np.stack(xs), np.stack(ts)
+        out[name + "_obj"] = np.array([e.objective for e in rep.epochs])
+        out[name + "_objmid"] = np.array([e.objective_mid for e in rep.epochs])
+        out[name + "_rmse"] = np.array([e.rmse for e in rep.epochs])
+        if name == "exact":
+            out["exact_mpr"] = np.array(imp.mean_percentile_rank(X, T, te))
+        print("implicit", name, out[name + "_obj"], out[name + "_rmse"])
+    np.savez_compressed(os.path.join(OUT, "implicit_small.npz"), **out)
+
+
 if __name__ == "__main__":
     cmf = import_reference()
     cmf.set_workers(os.cpu_count() or 1)
-    which = sys.argv[1:] or ["gram", "solve", "build", "data", "small", "ml1m"]
+    which = sys.argv[1:] or ["gram", "solve", "build", "data", "small", "implicit", "ml1m"]
     for w in which:
         {"gram": gram_cases, "solve": solve_cases, "build": build_cases,
-         "data": data_cases, "small": train_small, "ml1m": train_ml1m}[w](cmf)
+         "data": data_cases, "small": train_small, "implicit": implicit_small,
+         "ml1m": train_ml1m}[w](cmf)
         print("wrote", w)

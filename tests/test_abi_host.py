@@ -117,3 +117,12 @@ def test_model_file_roundtrip(tmp_path):
     (tmp_path / "bad").write_bytes(b"XXXX")
     with pytest.raises(cmfb.FormatError):
         cmfb.load_model(tmp_path / "bad")
+
+
+def test_implicit_config_validation():
+    import paper_1808_03843_b200 as cmfb
+    for kw in ({"f": 0}, {"alpha": 0.0}, {"lam": -1.0}, {"epochs": 0}):
+        with pytest.raises(cmfb.DataError):
+            cmfb.ImplicitConfig(**kw)
+    c = cmfb.ImplicitConfig()
+    assert (c.f, c.alpha, c.lam, c.epochs) == (100, 40.0, 0.05, 10)

@@ -1,0 +1,85 @@
+"""Implicit-feedback ALS (reference implicit.py) on the GPU vs the
+reference's own outputs (tests/golden/implicit_small.npz, made by
+tests/golden/make_golden.py from /root/reference).
+
+Bars, as for the explicit engine: the exact route holds the factors within
+1e-4 relative per half-update and epoch, the CG route holds the trajectory
+(preference RMSE) within 1e-3; objectives are float64 Gram-trick sums."""
+
+import numpy as np
+import pytest
+
+import paper_1808_03843_b200 as cmfb
+
+pytestmark = pytest.mark.gpu
+
+
+def _instance(g):
+    m, n, f = (int(v) for v in g["meta"])
+    sr = cmfb.SparseRatings(m, n, int(g["row_ptr"][-1]), g["row_ptr"], g["col_idx"], g["csr_val"],
+                            g["col_ptr"], g["row_idx"], g["csc_val"])
+    te = cmfb.Triples(g["te_u"], g["te_v"], g["te_r"])
+    return sr, te, f
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def test_precompute_gram_matches_reference(golden, cuda_device):
+    g = golden("implicit_small")
+    n, f = int(g["meta"][1]), int(g["meta"][2])
+    theta = cmfb.init_factors(n, f, 0.1, [0, 1])
+    assert _rel(cmfb.precompute_gram(theta), g["gram_theta"]) < 1e-6
+
+
+def test_implicit_update_side_exact(golden, cuda_device):
+    g = golden("implicit_small")
+    sr, _, f = _instance(g)
+    n = sr.n
+    theta = cmfb.init_factors(n, f, 0.1, [0, 1])
+    x = g["x0"].copy()
+    cmfb.implicit_update_side(sr.csr_view(), theta, g["gram_theta"], x, 40.0, 0.05,
+                              cmfb.SolverConfig("exact"))
+    assert _rel(x, g["x1_exact"]) < 1e-4
+    # users without observations: A = F^T F + lambda I, b = 0 -> exactly zero
+    assert np.all(x[-2:] == 0.0)
+
+
+@pytest.mark.parametrize("solver", ["exact", "cg32"])
+def test_implicit_train_trajectory(golden, cuda_device, solver):
+    g = golden("implicit_small")
+    sr, te, f = _instance(g)
+    cfg = cmfb.ImplicitConfig(f=f, alpha=40.0, lam=0.05, epochs=4,
+                              solver=cmfb.SolverConfig("exact") if solver == "exact"
+                              else cmfb.SolverConfig("cg", 6, 1e-4, "fp32"))
+    X, T, rep = cmfb.implicit_train(sr, cfg, te)
+    rmse = np.array([e.rmse for e in rep.epochs])
+    obj = np.array([e.objective for e in rep.epochs])
+    if solver == "exact":
+        assert _rel(X, g["exact_X"][-1]) < 1e-4 and _rel(T, g["exact_T"][-1]) < 1e-4
+        assert np.allclose(obj, g["exact_obj"], rtol=1e-5)
+        assert np.abs(rmse - g["exact_rmse"]).max() < 1e-5
+    else:
+        assert np.abs(rmse - g[solver + "_rmse"]).max() < 1e-3
+        assert np.allclose(obj, g[solver + "_obj"], rtol=1e-3)
+    assert rep.engine == "implicit" and len(rep.epochs) == 4
+
+
+def test_mean_percentile_rank_matches_reference(golden, cuda_device):
+    g = golden("implicit_small")
+    _, te, _ = _instance(g)
+    mpr = cmfb.mean_percentile_rank(g["exact_X"][-1], g["exact_T"][-1], te)
+    assert abs(mpr - float(g["exact_mpr"])) < 1e-6
+
+
+def test_implicit_fp16_overflow_and_negative_ratings(golden, cuda_device):
+    g = golden("implicit_small")
+    sr, te, f = _instance(g)
+    cfg = cmfb.ImplicitConfig(f=f, epochs=1, solver=cmfb.SolverConfig("cg", precision="fp16"))
+    with pytest.raises(cmfb.NumericalError):
+        cmfb.implicit_train(sr, cfg, te)
+    bad = cmfb.SparseRatings(sr.m, sr.n, sr.nnz, sr.row_ptr, sr.col_idx, -sr.csr_val, sr.col_ptr,
+                             sr.row_idx, -sr.csc_val)
+    with pytest.raises(cmfb.DataError):
+        cmfb.implicit_train(bad, cfg, te)
