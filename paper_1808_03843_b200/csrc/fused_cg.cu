@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
             float* const tgt = g.target + u * f;
             float xi = act ? tgt[i] : 0.0f;  // warm start, loaded while the Gram is built
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 0);
-            mbar_wait_backoff(pp.tfull(b), (r_here / NBUF) & 1);  // sleeps: long rows keep the group idle
+            mbar_wait_backoff<64, 4096>(pp.tfull(b), (r_here / NBUF) & 1);  // long rows keep the group idle
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 1);
             tc_fence_after();
             // A_u (fp32, thread i <-> lane i <-> row i) -> binary16 in place: columns

@@ -59,9 +59,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
     } while (!ok);
 }
 // Same, but spinning with plain try_wait and a nanosleep backoff: for waiters
-// that are not latency critical (producers facing a full ring).
+// that are not latency critical (producers facing a full ring; CG groups
+// waiting for long rows use a longer cap so idle warps stay off the issue slots).
+template <uint32_t NS0 = 32, uint32_t NSMAX = 512>
 __device__ __forceinline__ void mbar_wait_backoff(uint32_t a, uint32_t parity) {
-    uint32_t ok = 0, ns = 32;
+    uint32_t ok = 0, ns = NS0;
     while (true) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -72,7 +74,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint32_t a, uint32_t parity) {
             : "memory");
         if (ok) return;
         __nanosleep(ns);
-        if (ns < 512) ns <<= 1;
+        if (ns < NSMAX) ns <<= 1;
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -286,14 +288,18 @@ __device__ void produce(const GatherArgs &g, const __half *fixed16, const __half
     StageIter cur{0, 0, 0, g.nrows, rstride, g.indptr};
     cur.first(row0);
     cur.advance(pw);
-    StageIter n1 = cur;
-    n1.advance(nprod);
-    StageIter n2 = n1;
-    n2.advance(nprod);
-    StagePairs c0, c1, c2;
-    c0.load(g, cur, lane);
-    c1.load(g, n1, lane);
-    c2.load(g, n2, lane);
+    // three in-flight stages in a static ring: slot k always holds its own
+    // registers (no register moves), so the index/rating loads issued for a
+    // stage are not waited on until that stage is produced
+    StageIter st[3];
+    st[0] = cur;
+    st[1] = st[0];
+    st[1].advance(nprod);
+    st[2] = st[1];
+    st[2].advance(nprod);
+    StagePairs q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) q[k].load(g, st[k], lane);
     const int c = lane & 15, hrow = lane >> 4;
     const bool live = c < (W >> 3);
     const uint32_t W2 = static_cast<uint32_t>(W) * 2;
@@ -309,9 +315,9 @@ __device__ void produce(const GatherArgs &g, const __half *fixed16, const __half
 #pragma unroll
     for (int h = 0; h < 2; ++h) r_off[h] = operand_addr(0, 32 * h + lane, W >> 3);
     uint32_t it = pw;
-    while (cur.valid()) {
+    auto stage_out = [&](const StageIter &cs, StagePairs &c0) {
         const int s = it % NST;
-        const int nrem16 = static_cast<int>(min(static_cast<int64_t>(KS), cur.p1 - cur.q0) + 15) & ~15;
+        const int nrem16 = static_cast<int>(min(static_cast<int64_t>(KS), cs.p1 - cs.q0) + 15) & ~15;
         c0.clamp_ids(g.ncols);
         if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 0);
         mbar_wait_backoff(pp.empty(s), ((it / NST) & 1) ^ 1);
@@ -347,13 +353,25 @@ __device__ void produce(const GatherArgs &g, const __half *fixed16, const __half
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(pp.full(s)) : "memory");
         if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 2);
-        cur = n1;
-        n1 = n2;
-        n2.advance(nprod);
-        c0 = c1;
-        c1 = c2;
-        c2.load(g, n2, lane);
         it += nprod;
+    };
+    // slot k's next stage is three of this warp's stages on: the stage after slot (k+2)'s
+    while (true) {
+        if (!st[0].valid()) break;
+        stage_out(st[0], q[0]);
+        st[0] = st[2];
+        st[0].advance(nprod);
+        q[0].load(g, st[0], lane);
+        if (!st[1].valid()) break;
+        stage_out(st[1], q[1]);
+        st[1] = st[0];
+        st[1].advance(nprod);
+        q[1].load(g, st[1], lane);
+        if (!st[2].valid()) break;
+        stage_out(st[2], q[2]);
+        st[2] = st[1];
+        st[2].advance(nprod);
+        q[2].load(g, st[2], lane);
     }
 }
 
