@@ -491,7 +491,9 @@ def e2e(cmfb, train, x0, th0, solver, args):
     torch.cuda.synchronize()
     v = (time.perf_counter() - t0) / steps
     return {"value": v, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "paper_1808_03843_b200.update_side x2 (C ABI via ctypes), pinned host buffers"}
+            "pcie_gbs": (h2d + d2h) / v / 1e9,
+            "api": "paper_1808_03843_b200.update_side x2 (C ABI via ctypes), pinned host buffers; "
+                   "copies of chunk k+1 / k-1 overlap the fused kernel on chunk k"}
 
 
 if __name__ == "__main__":

@@ -142,6 +142,7 @@ class HalfUpdatePlan:
         self.flags = torch.zeros(4, dtype=torch.int32, device=dev)
         self.w16 = nat.tc_width(f)
         self.shadow = None  # binary16 copy of the fixed factors (tensor-core Gram)
+        self._shadow_lo = None
 
     def _workspace(self):
         if self.a_ws is None:
@@ -170,7 +171,7 @@ class HalfUpdatePlan:
         return self.shadow, None
 
     def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
-               row0: int = 0, nrows: int | None = None):
+               row0: int = 0, nrows: int | None = None, reuse_shadow: bool = False):
         """Gram(+bias) -> solve for rows [row0, row0+nrows) of the view, block by
         block, solutions written into tg (rows indexed like the view)."""
         f, solver = self.f, self.solver
@@ -180,7 +181,11 @@ class HalfUpdatePlan:
         if record is not None and tc:
             es0 = torch.cuda.Event(enable_timing=True)
             es0.record()
-        shadow, lo = self._shadow(fx, split=kernel == "tc_split") if tc else (None, None)
+        if tc and reuse_shadow and self.shadow is not None:  # same fixed factors as the last call
+            shadow, lo = self.shadow, self._shadow_lo
+        else:
+            shadow, lo = self._shadow(fx, split=kernel == "tc_split") if tc else (None, None)
+            self._shadow_lo = lo
         if record is not None and tc:
             es1 = torch.cuda.Event(enable_timing=True)
             es1.record()
@@ -261,6 +266,10 @@ def update_side(view: RowView, fixed, target, lam: float, solver: SolverConfig,
     kernel = resolve_gram_kernel(gram_kernel, solver, int(fixed.shape[1]))
     host = not nat.is_device(target)
     dev = nat.device()
+    if (host and kernel == "tc" and solver.method == "cg"
+            and _all_pinned(view.indptr, view.indices, view.values, fixed, target)
+            and int(view.nrows) >= STREAM_MIN_ROWS):
+        return _update_side_streamed(view, fixed, target, lam, solver, weighted_reg, dev)
     indptr, indices, values = _view_dev(view, dev)
     fx = nat.to_dev(fixed, torch.float32, dev)
     tg = nat.to_dev(target, torch.float32, dev) if host else target
@@ -291,6 +300,76 @@ def update_side(view: RowView, fixed, target, lam: float, solver: SolverConfig,
             target.copy_(tg)
         else:
             target[...] = nat.to_host(tg)
+    return times, nrows * packed_size(f) * plan.esize, int(fl[1])
+
+
+STREAM_CHUNKS = int(os.environ.get("CMF_STREAM_CHUNKS", "8"))
+STREAM_MIN_ROWS = 4096
+
+
+def _all_pinned(*ts) -> bool:
+    return all(isinstance(t, torch.Tensor) and t.device.type == "cpu" and t.is_pinned() and t.is_contiguous()
+               for t in ts)
+
+
+def _update_side_streamed(view: RowView, fixed, target, lam, solver, weighted_reg, dev):
+    """update_side for pinned host buffers on the fused CG route, with the PCIe
+    transfers overlapped: the fixed factors and indptr go first, then the rows
+    are cut into STREAM_CHUNKS nnz-balanced chunks; chunk k's indices / ratings
+    / warm start are copied on a copy stream while the fused kernel solves chunk
+    k-1, and each solved chunk of ``target`` is copied back on a third stream.
+    Same results as the unchunked call (each row's system is independent)."""
+    f = int(fixed.shape[1])
+    nrows = int(view.nrows)
+    comp = torch.cuda.current_stream(dev)
+    h2d = torch.cuda.Stream(dev)
+    d2h = torch.cuda.Stream(dev)
+    indptr_h = view.indptr.to(torch.int64) if view.indptr.dtype != torch.int64 else view.indptr
+    ptr_np = indptr_h.numpy()
+    nnz = int(ptr_np[-1])
+    k = max(1, min(STREAM_CHUNKS, nrows // 1024))
+    cuts = np.searchsorted(ptr_np, np.linspace(0, nnz, k + 1)[1:-1], side="left")
+    bounds = np.unique(np.concatenate([[0], cuts, [nrows]]))
+    indptr = torch.empty(nrows + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(nnz, dtype=torch.int32, device=dev)
+    values = torch.empty(nnz, dtype=torch.float32, device=dev)
+    fx = torch.empty(fixed.shape, dtype=torch.float32, device=dev)
+    tg = torch.empty(target.shape, dtype=torch.float32, device=dev)
+    plan = HalfUpdatePlan(nrows, f, solver, dev)
+    with torch.cuda.stream(h2d):
+        fx.copy_(fixed, non_blocking=True)
+        indptr.copy_(indptr_h, non_blocking=True)
+        ev_base = torch.cuda.Event()
+        ev_base.record(h2d)
+        evs = []
+        for r0, r1 in zip(bounds[:-1], bounds[1:]):
+            p0, p1 = int(ptr_np[r0]), int(ptr_np[r1])
+            indices[p0:p1].copy_(view.indices[p0:p1], non_blocking=True)
+            values[p0:p1].copy_(view.values[p0:p1], non_blocking=True)
+            tg[r0:r1].copy_(target[r0:r1], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(h2d)
+            evs.append(e)
+    comp.wait_event(ev_base)
+    rec = {}
+    for ci, (r0, r1) in enumerate(zip(bounds[:-1], bounds[1:])):
+        comp.wait_event(evs[ci])
+        plan.launch(indptr, indices, values, fx, tg, lam, weighted_reg, "tc", rec,
+                    row0=int(r0), nrows=int(r1 - r0), reuse_shadow=ci > 0)
+        done = torch.cuda.Event()
+        done.record(comp)
+        d2h.wait_event(done)
+        with torch.cuda.stream(d2h):
+            target[r0:r1].copy_(tg[r0:r1], non_blocking=True)
+    # keep the device buffers alive until the copies that use them have run
+    for t in (indptr, indices, values, fx, tg):
+        t.record_stream(h2d)
+        t.record_stream(d2h)
+    d2h.synchronize()
+    fl = plan.read_flags()
+    times = PhaseTimes()
+    for name, ms in resolve_events(rec).items():
+        times.accumulate += sum(ms) / 1e3
     return times, nrows * packed_size(f) * plan.esize, int(fl[1])
 
 
