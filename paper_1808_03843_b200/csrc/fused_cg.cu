@@ -152,6 +152,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t *v) {
         "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // D[tmem] (+)= A[tmem] * B[smem]: kind::f16, A operand read from tensor memory
 __device__ __forceinline__ void tc_mma_tmem_a(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
@@ -181,6 +186,155 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     return v;
 }
 
+// Truncated CG on one system whose binary16 matrix sits in TMEM (thread i <->
+// lane i <-> row i; the tcgen05 A-operand layout: column j holds elements
+// 2j, 2j+1), run by one 128-thread group (4 warps, one named barrier).
+//
+// The reference's Algorithm 1 (solvers.py:83-118, corrected
+// r -= alpha*A p) in its pipelined (Ghysels-Vanroose) form: s = A p, z = A s,
+// w = A r are carried by recurrences, so each iteration needs ONE exchange --
+// thread i publishes its vector entry (fp16 hi/lo into a K-major smem operand)
+// and the warp sums of (r.r, w.r); after the barrier one thread issues the
+// matvec on the tensor core (A from TMEM, N = 16, result in TMEM) while every
+// thread finishes the sums.  Semantics: at least one update unless
+// p^T A p <= 0 (breakdown: x kept), stop once ||r|| < eps, `nit` counts the
+// x updates.  Deterministic (fixed reduction order).
+template <int KP>
+struct TmemCg {
+    static constexpr int NKS = KP / 16;  // kind::f16 MMAs per matvec
+    uint32_t bop, bofs0, bofs1, mvbar, lane_base;
+    float *red;
+    uint32_t mvph = 0;
+    int slot = 0, bar_id, i, lane, warp;
+    bool leader, act;
+
+    __device__ TmemCg(unsigned char *scratch, uint32_t mvbar_, int bar_id_, int warp_, int lane_, int f)
+        : bop(smem_u32(scratch)), mvbar(mvbar_), bar_id(bar_id_), lane(lane_), warp(warp_) {
+        i = (warp & 3) * 32 + lane;
+        act = i < f;
+        red = reinterpret_cast<float *>(scratch + MVB_OPERAND);
+        // B(n, k): n = 0 / 1 hold the vector's fp16 hi / lo halves at K position k = i
+        bofs0 = (i / 64) * 2048 + ((((i % 64) >> 3) ^ 0) << 4) + (i & 7) * 2;
+        bofs1 = (i / 64) * 2048 + 128 + ((((i % 64) >> 3) ^ 1) << 4) + (i & 7) * 2;
+        leader = (warp & 3) == 0;
+        lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    }
+
+    // y_i = (A v)_i + reg * v_i and (sa, sb) = group sums of (da, db); rows i >= f
+    // (act == false) publish nothing and return 0
+    __device__ float exchange(uint32_t a_tmem, uint32_t dcol, float reg, float v, float da, float db, float &sa,
+                              float &sb, bool mv) {
+        constexpr uint32_t idesc_mv = (1u << 4) | (static_cast<uint32_t>(16 >> 3) << 17) |
+                                      (static_cast<uint32_t>(128 >> 4) << 24);  // f16 x f16 -> f32, K-major
+        if (mv && act) {
+            const __half hv = __float2half_rn(v);
+            const __half lv = __float2half_rn(v - __half2float(hv));
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(bop + bofs0), "h"(__half_as_ushort(hv)) : "memory");
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(bop + bofs1), "h"(__half_as_ushort(lv)) : "memory");
+        }
+        if (mv) fence_proxy_async();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            da += __shfl_xor_sync(0xffffffffu, da, o);
+            db += __shfl_xor_sync(0xffffffffu, db, o);
+        }
+        float *rd = red + 8 * slot;
+        slot ^= 1;
+        if (lane == 0) {
+            rd[warp & 3] = da;
+            rd[4 + (warp & 3)] = db;
+        }
+        named_bar(bar_id, CG_THREADS);
+        if (mv && leader) {
+            if (elect_one()) {
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < NKS; ++kk)
+                    tc_mma_tmem_a(dcol, a_tmem + 8 * kk, make_desc_kmajor(bop + (kk >> 2) * 2048 + (kk & 3) * 32),
+                                  idesc_mv, kk);
+                tc_commit(mvbar);
+            }
+            __syncwarp();
+        }
+        sa = (rd[0] + rd[1]) + (rd[2] + rd[3]);
+        sb = (rd[4] + rd[5]) + (rd[6] + rd[7]);
+        if (!mv) return 0.0f;
+        mbar_wait(mvbar, mvph & 1);
+        ++mvph;
+        tc_fence_after();
+        const float y0 = __uint_as_float(tmem_ld1(dcol + lane_base));
+        const float y1 = __uint_as_float(tmem_ld1(dcol + lane_base + 1));
+        tmem_ld_wait();
+        const float y = act ? y0 + y1 : 0.0f;
+        return fmaf(reg, v, y);
+    }
+
+    // The same solve with the standard recurrence (explicit p^T A p and r.r
+    // reductions, three barriers per iteration): the per-system accuracy the
+    // reference-facing batch_solve is held to on ill-conditioned systems.
+    __device__ void solve_standard(uint32_t a_tmem, uint32_t dcol, float bi, double eps, float tol, int f_s,
+                                   float &xi, int &bd, int &nit) {
+        float bb, rs, unused;
+        float r = bi - exchange(a_tmem, dcol, 0.0f, xi, bi * bi, 0.0f, bb, unused, true);
+        const double e = eps >= 0.0 ? eps : static_cast<double>(tol) * sqrt(static_cast<double>(bb));
+        exchange(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs, unused, false);
+        float p = r;
+        bd = 0;
+        nit = 0;
+        for (int step = 0; step < f_s; ++step) {
+            float pap, rs_new;
+            const float ap = exchange(a_tmem, dcol, 0.0f, p, 0.0f, 0.0f, unused, unused, true);
+            exchange(a_tmem, dcol, 0.0f, 0.0f, p * ap, 0.0f, pap, unused, false);
+            if (!(pap > 0.0f)) {
+                bd = 1;
+                break;
+            }
+            const float alpha = rs / pap;
+            xi = fmaf(alpha, p, xi);
+            r = fmaf(-alpha, ap, r);
+            exchange(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs_new, unused, false);
+            ++nit;
+            if (rs_new == 0.0f || sqrt(static_cast<double>(rs_new)) < e) break;
+            p = fmaf(rs_new / rs, p, r);
+            rs = rs_new;
+        }
+    }
+
+    // solve (A + reg I) x = b from the warm start xi; eps < 0: eps = tol * ||b||
+    __device__ void solve(uint32_t a_tmem, uint32_t dcol, float reg, float bi, double eps, float tol, int f_s,
+                          float &xi, int &bd, int &nit) {
+        float bb, unused;
+        float r = bi - exchange(a_tmem, dcol, reg, xi, bi * bi, 0.0f, bb, unused, true);
+        const float eps2 = eps >= 0.0 ? static_cast<float>(eps * eps) : tol * tol * bb;
+        float gamma, delta;
+        float w = exchange(a_tmem, dcol, reg, r, 0.0f, 0.0f, gamma, delta, true);
+        float p = 0.0f, sv = 0.0f, z = 0.0f, gamma_old = 1.0f, alpha_old = 1.0f;
+        bd = 0;
+        nit = 0;
+        for (int step = 0; step < f_s; ++step) {
+            const bool last = step + 1 >= f_s;
+            const float m = exchange(a_tmem, dcol, reg, w, r * r, w * r, gamma, delta, !last);
+            if (step > 0 && (gamma == 0.0f || gamma < eps2)) break;
+            const float beta = step > 0 ? gamma * __frcp_rn(gamma_old) : 0.0f;
+            const float pap = step > 0 ? delta - beta * gamma * __frcp_rn(alpha_old) : delta;
+            if (!(pap > 0.0f)) {
+                bd = 1;
+                break;
+            }
+            const float alpha = gamma * __frcp_rn(pap);
+            z = fmaf(beta, z, m);
+            sv = fmaf(beta, sv, w);
+            p = fmaf(beta, p, r);
+            xi = fmaf(alpha, p, xi);
+            r = fmaf(-alpha, sv, r);
+            w = fmaf(-alpha, z, w);
+            gamma_old = gamma;
+            alpha_old = alpha;
+            ++nit;
+        }
+    }
+};
+
 // FC = ceil(f/4): register row of A_u as FC*2 float2 pairs.
 template <int FC>
 __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(const __grid_constant__ FusedArgs g) {
@@ -190,7 +344,6 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
     constexpr int NBUF = FusedShape<FC>::NBUF;
     using PipeT = FPipe<NBUF>;
     constexpr int KP = (FC * 4 + 15) / 16 * 16;  // matvec K extent (>= f), 16-half MMA steps
-    constexpr int NKS = KP / 16;                  // kind::f16 MMAs per matvec
     constexpr int F_STAGES = PipeT::kStages;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const GatherArgs &ga = g.gather;
@@ -245,22 +398,10 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
         // ------------------------------------------------------------ CG groups
         const int grp = warp >> 2;             // rows r with r % NG == grp
         const int i = (warp & 3) * 32 + lane;  // row of A_u == TMEM lane
-        const int bar_id = 1 + grp;
-        unsigned char *mine_s = scratch + grp * MVB_BYTES;
-        const uint32_t bop = smem_u32(mine_s);               // matvec B operand (K-major SW128)
-        float *red = reinterpret_cast<float *>(mine_s + MVB_OPERAND);  // 2 x 8 warp partials
-        const uint32_t mvbar = smem_u32(mvbars + grp);
-        // B(n, k): n = 0 / 1 hold the vector's fp16 hi / lo halves at K position k = i
-        const uint32_t bofs0 = (i / 64) * 2048 + ((((i % 64) >> 3) ^ 0) << 4) + (i & 7) * 2;
-        const uint32_t bofs1 = (i / 64) * 2048 + 128 + ((((i % 64) >> 3) ^ 1) << 4) + (i & 7) * 2;
-        const bool act = i < f;
-        const bool leader = (warp & 3) == 0;  // issues the group's matvec MMAs
-        constexpr uint32_t idesc_mv = (1u << 4) | (static_cast<uint32_t>(16 >> 3) << 17) |
-                                      (static_cast<uint32_t>(128 >> 4) << 24);  // f16 x f16 -> f32, K-major
+        TmemCg<KP> cg(scratch + grp * MVB_BYTES, smem_u32(mvbars + grp), 1 + grp, warp, lane, f);
+        const bool act = cg.act;
         int32_t brk = 0;
         uint32_t rowc = 0;    // non-empty rows of this CTA so far (all groups)
-        uint32_t mvph = 0;    // matvec barrier phase
-        int slot = 0;         // reduction buffers alternate
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
             const int64_t p0 = ga.indptr[u];
@@ -305,92 +446,8 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
             const uint32_t a_tmem = tmem_base + b * g.N;
             const float reg = g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
                                          : __double2float_rn(g.lam);
-            // One barrier per exchange: thread i publishes its entry of the vector
-            // (fp16 hi/lo into the B operand) and the warp sums of two dot
-            // products; after the barrier one thread issues the matvec on the
-            // tensor core (A from TMEM) while every thread finishes the sums.
-            //   y_i = (A_u v)_i + reg * v_i,  (sa, sb) = group sums of (da, db)
-            int ev = 0;
-            auto exchange = [&](float v, float da, float db, float &sa, float &sb, bool mv) -> float {
-                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
-                if (mv && act) {
-                    const __half hv = __float2half_rn(v);
-                    const __half lv = __float2half_rn(v - __half2float(hv));
-                    asm volatile("st.shared.b16 [%0], %1;" ::"r"(bop + bofs0), "h"(__half_as_ushort(hv)) : "memory");
-                    asm volatile("st.shared.b16 [%0], %1;" ::"r"(bop + bofs1), "h"(__half_as_ushort(lv)) : "memory");
-                }
-                if (mv) fence_proxy_async();
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    da += __shfl_xor_sync(0xffffffffu, da, o);
-                    db += __shfl_xor_sync(0xffffffffu, db, o);
-                }
-                float *rd = red + 8 * slot;
-                slot ^= 1;
-                if (lane == 0) {
-                    rd[warp & 3] = da;
-                    rd[4 + (warp & 3)] = db;
-                }
-                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
-                named_bar(bar_id, CG_THREADS);
-                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
-                if (mv && leader) {
-                    if (elect_one()) {
-                        tc_fence_after();
-#pragma unroll
-                        for (int kk = 0; kk < NKS; ++kk)
-                            tc_mma_tmem_a(dcol, a_tmem + 8 * kk,
-                                          make_desc_kmajor(bop + (kk >> 2) * 2048 + (kk & 3) * 32), idesc_mv, kk);
-                        tc_commit(mvbar);
-                    }
-                    __syncwarp();
-                }
-                sa = (rd[0] + rd[1]) + (rd[2] + rd[3]);
-                sb = (rd[4] + rd[5]) + (rd[6] + rd[7]);
-                if (!mv) return 0.0f;
-                mbar_wait(mvbar, mvph & 1);
-                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
-                ++mvph;
-                tc_fence_after();
-                const float y0 = __uint_as_float(tmem_ld1(dcol + lane_base));
-                const float y1 = __uint_as_float(tmem_ld1(dcol + lane_base + 1));
-                tmem_ld_wait();
-                const float y = act ? y0 + y1 : 0.0f;
-                if (i == 0 && r_here < 64) trace_at(ga.trace, 40960 + 64 * r_here + (ev++ & 63));
-                return fmaf(reg, v, y);
-            };
-            // Pipelined CG (Ghysels & Vanroose): the same iterates as Algorithm 1
-            // in exact arithmetic; s = A p, z = A s, w = A r are carried by
-            // recurrences, so each iteration needs ONE exchange: (r.r, w.r) and
-            // m = A w together.  Semantics as the reference: at least one update
-            // unless p^T A p <= 0 (breakdown, x kept); stop once ||r|| < eps.
-            float bb, unused;
-            float r = bi - exchange(xi, bi * bi, 0.0f, bb, unused, true);
-            const float eps2 = g.tol * g.tol * bb;
-            float gamma, delta;
-            float w = exchange(r, 0.0f, 0.0f, gamma, delta, true);
-            float p = 0.0f, sv = 0.0f, z = 0.0f, gamma_old = 1.0f, alpha_old = 1.0f;
-            int bd = 0;
-            for (int step = 0; step < g.f_s; ++step) {
-                const bool last = step + 1 >= g.f_s;
-                const float m = exchange(w, r * r, w * r, gamma, delta, !last);
-                if (step > 0 && (gamma == 0.0f || gamma < eps2)) break;
-                const float beta = step > 0 ? gamma * __frcp_rn(gamma_old) : 0.0f;
-                const float pap = step > 0 ? delta - beta * gamma * __frcp_rn(alpha_old) : delta;
-                if (!(pap > 0.0f)) {
-                    bd = 1;
-                    break;
-                }
-                const float alpha = gamma * __frcp_rn(pap);
-                z = fmaf(beta, z, m);
-                sv = fmaf(beta, sv, w);
-                p = fmaf(beta, p, r);
-                xi = fmaf(alpha, p, xi);
-                r = fmaf(-alpha, sv, r);
-                w = fmaf(-alpha, z, w);
-                gamma_old = gamma;
-                alpha_old = alpha;
-            }
+            int bd = 0, nit = 0;
+            cg.solve(a_tmem, dcol, reg, bi, -1.0, g.tol, g.f_s, xi, bd, nit);
             tc_fence_before();
             mbar_arrive(pp.tempty(b));  // the accumulator is free for row r_here + NBUF
             if (act) tgt[i] = xi;
@@ -404,6 +461,138 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
     if (warp == F_MMA_WARP) {
         tc_fence_after();
         tmem_dealloc(tmem_base, g.tmem_cols);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Batched CG over packed binary16 systems (the two-step route's K3: replaces
+// solvers._cg_batch for precision="fp16", solvers.py:121-145, 205-247).
+// Three 128-thread groups per CTA, two CTAs per SM; each group double-buffers
+// its systems' packed lower triangles HBM -> shared memory with cp.async
+// (the only large read), expands row i of the symmetric matrix into its TMEM
+// slot in the tcgen05 A-operand layout (the stored binary16 values, no
+// rounding), and runs TmemCg (tensor-core matvecs, one barrier per iteration).
+struct CgTcArgs {
+    const __half *a;
+    int64_t a_stride;  // halves, 8-aligned
+    const float *b, *x0;
+    const double *eps;
+    double tol;
+    const int64_t *nu;
+    int64_t nsys;
+    int f, f_s;
+    float *x_out;
+    int32_t *iters, *broke, *breakdowns;
+    int pipelined;  // CMF_CG_PIPELINED=1: one barrier per iteration (pipelined recurrence)
+};
+
+constexpr int CGT_GROUPS = 3;
+constexpr int CGT_THREADS = 128 * CGT_GROUPS;
+
+template <int KP>
+__global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_constant__ CgTcArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    const int f = g.f;
+    const int64_t P = packed_size(f);
+    const int SB = static_cast<int>((P * 2 + 127) & ~127ll);  // staging bytes per system
+    // per-group scratch: the matvec operand must sit on a 1024-byte swizzle atom
+    const int GS = (MVB_BYTES + 2 * SB + 1023) & ~1023;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = warp >> 2;
+    unsigned char *scr = smem + grp * GS;
+    unsigned char *stg = scr + MVB_BYTES;
+    uint64_t *mvbars = reinterpret_cast<uint64_t *>(smem + CGT_GROUPS * GS);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mvbars + CGT_GROUPS);
+    for (int k = tid; k < CGT_GROUPS * GS / 16; k += CGT_THREADS)
+        reinterpret_cast<int4 *>(smem)[k] = make_int4(0, 0, 0, 0);
+    if (tid == 0) {
+        for (int q = 0; q < CGT_GROUPS; ++q) mbar_init(smem_u32(mvbars + q), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    TmemCg<KP> cg(scr, smem_u32(mvbars + grp), 1 + grp, warp, lane, f);
+    const int i = cg.i, gt = tid & 127;
+    // TMEM: 16-column aligned slots (KP/2 packed columns each), then the 16-column
+    // matvec results from a 32-column boundary
+    constexpr uint32_t SLOT = (KP / 2 + 15) / 16 * 16;
+    constexpr uint32_t DBASE = (CGT_GROUPS * SLOT + 31) / 32 * 32;
+    static_assert(DBASE + 16 * CGT_GROUPS <= 256, "cg_tc TMEM plan");
+    const uint32_t a_tmem = tmem_base + grp * SLOT;
+    const uint32_t dcol = tmem_base + DBASE + 16 * grp;
+    const uint32_t slot_t = a_tmem + cg.lane_base;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * CGT_GROUPS;
+    const int nchunk = static_cast<int>((P * 2 + 15) / 16);  // within a_stride (8-aligned) of each system
+    auto stage = [&](int64_t sys, int buf) {
+        if (sys < g.nsys && !(g.nu && g.nu[sys] == 0)) {
+            const char *src = reinterpret_cast<const char *>(g.a + sys * g.a_stride);
+            unsigned char *dst = stg + buf * SB;
+            for (int k = gt; k < nchunk; k += 128) cp_async16(dst + 16 * k, src + 16 * k);
+        }
+        cp_async_commit();
+    };
+    int32_t brk = 0;
+    int buf = 0;
+    int64_t sys = static_cast<int64_t>(blockIdx.x) * CGT_GROUPS + grp;
+    stage(sys, 0);
+    for (; sys < g.nsys; sys += stride, buf ^= 1) {
+        stage(sys + stride, buf ^ 1);  // next system in flight while this one is solved
+        if (g.nu && g.nu[sys] == 0) continue;
+        const bool act = cg.act;
+        float xi = act ? g.x0[sys * f + i] : 0.0f;
+        const float bi = act ? g.b[sys * f + i] : 0.0f;
+        cp_async_wait<1>();
+        named_bar(1 + grp, CG_THREADS);
+        // row i of the symmetric matrix -> binary16 pairs in TMEM
+        const __half *A = reinterpret_cast<const __half *>(stg + buf * SB);
+        const int64_t ri = static_cast<int64_t>(i) * (i + 1) / 2;
+#pragma unroll 1
+        for (int c = 0; c < (KP + 31) / 32; ++c) {
+            uint32_t h[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                uint16_t e[2];
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int j = 32 * c + 2 * q + t;
+                    uint16_t v = 0;
+                    if (act && j < f)
+                        v = __half_as_ushort(j <= i ? A[ri + j] : A[static_cast<int64_t>(j) * (j + 1) / 2 + i]);
+                    e[t] = v;
+                }
+                h[q] = static_cast<uint32_t>(e[0]) | (static_cast<uint32_t>(e[1]) << 16);
+            }
+            if (16 * c + 16 <= KP / 2) tmem_st16(slot_t + 16 * c, h);
+            else if (16 * c < KP / 2) tmem_st8(slot_t + 16 * c, h);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        int bd = 0, nit = 0;
+        if (g.pipelined)
+            cg.solve(a_tmem, dcol, 0.0f, bi, g.eps ? g.eps[sys] : -1.0, static_cast<float>(g.tol), g.f_s, xi, bd,
+                     nit);
+        else
+            cg.solve_standard(a_tmem, dcol, bi, g.eps ? g.eps[sys] : -1.0, static_cast<float>(g.tol), g.f_s, xi,
+                              bd, nit);
+        if (act) g.x_out[sys * f + i] = xi;
+        if (gt == 0) {
+            if (g.iters) g.iters[sys] = nit;
+            if (g.broke) g.broke[sys] = bd;
+        }
+        brk += bd;
+        tc_fence_before();  // the next system's repack overwrites the slot the MMAs read
+    }
+    cp_async_wait<0>();
+    if (gt == 0 && brk && g.breakdowns) atomicAdd(g.breakdowns, brk);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 256);
     }
 }
 
@@ -492,5 +681,47 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
     return set_error(CMF_EINVAL, "no fused CG instance for f=%d", f);
 }
 #undef CMF_FUSED_CASE
+
+template <int KP>
+static int launch_cg_tc(const tc::CgTcArgs &g, cudaStream_t st) {
+    const int64_t P = packed_size(g.f);
+    const size_t SB = (P * 2 + 127) & ~127ll;
+    const size_t GS = (tc::MVB_BYTES + 2 * SB + 1023) & ~static_cast<size_t>(1023);
+    const size_t smem = 1024 + tc::CGT_GROUPS * GS + tc::CGT_GROUPS * 8 + 16;
+    auto k = tc::cg_tc_kernel<KP>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return set_error(CMF_ECUDA, "cg_tc smem attr: %s", cudaGetErrorString(e));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = 2 * static_cast<int64_t>(sms);
+    const int64_t need = (g.nsys + tc::CGT_GROUPS - 1) / tc::CGT_GROUPS;
+    if (grid > need) grid = need;
+    k<<<static_cast<unsigned>(grid), tc::CGT_THREADS, smem, st>>>(g);
+    return check_launch("cg_tc_kernel");
+}
+
+// fp16 batched CG on the tensor cores; returns -1 when the shape is not covered
+// (the caller then uses the SIMT kernel): f <= 120, 16-byte aligned rows.
+int cg_tc_launch(const void *a, int64_t a_stride, const float *b, const float *x0, const double *eps, double tol,
+                 const int64_t *nu, int64_t nsys, int f, int f_s, float *x_out, int32_t *iters, int32_t *broke,
+                 int32_t *breakdowns, cudaStream_t st) {
+    if (f > 120 || (a_stride % 8) != 0 || (reinterpret_cast<uintptr_t>(a) & 15) != 0) return -1;
+    if (nsys == 0) return CMF_OK;
+    const char *pe = getenv("CMF_CG_PIPELINED");
+    tc::CgTcArgs g{static_cast<const __half *>(a), a_stride, b, x0, eps, tol, nu, nsys, f, f_s, x_out, iters,
+                   broke, breakdowns, pe ? atoi(pe) : 0};
+    const int kp = (f + 15) / 16 * 16;
+    switch (kp) {
+        case 16: return launch_cg_tc<16>(g, st);
+        case 32: return launch_cg_tc<32>(g, st);
+        case 48: return launch_cg_tc<48>(g, st);
+        case 64: return launch_cg_tc<64>(g, st);
+        case 80: return launch_cg_tc<80>(g, st);
+        case 96: return launch_cg_tc<96>(g, st);
+        case 112: return launch_cg_tc<112>(g, st);
+        default: return launch_cg_tc<128>(g, st);
+    }
+}
 
 }  // namespace cmf

@@ -339,6 +339,9 @@ static int dispatch_rowreg(const CgArgs &g, cudaStream_t st) {
     return launch_rowreg<32, H>(g, st);
 }
 
+int cg_tc_launch(const void *, int64_t, const float *, const float *, const double *, double, const int64_t *,
+                 int64_t, int, int, float *, int32_t *, int32_t *, int32_t *, cudaStream_t);
+
 int cg_launch(const void *a, bool half, int64_t a_stride, const float *b, const float *x0,
               const double *eps, double tol, const int64_t *nu, int64_t nsys, int f, int f_s,
               bool fp64, float *x_out, int32_t *iters, int32_t *broke, int32_t *breakdowns,
@@ -361,6 +364,11 @@ int cg_launch(const void *a, bool half, int64_t a_stride, const float *b, const 
     g.breakdowns = breakdowns;
     const size_t es = half ? 2 : 4;
     g.vec16 = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && ((a_stride * es) % 16 == 0);
+    if (half && !fp64) {  // fp16 storage: tensor-core CG (A in TMEM) when the shape allows
+        const int rc = cg_tc_launch(a, a_stride, b, x0, eps, tol, nu, nsys, f, f_s, x_out, iters, broke,
+                                    breakdowns, st);
+        if (rc >= 0) return rc;
+    }
     if (!fp64 && f <= 128) return half ? dispatch_rowreg<true>(g, st) : dispatch_rowreg<false>(g, st);
     // float64 (reference-exact) path, also the fallback for f > 128
     int nt = ((f + 31) / 32) * 32;
