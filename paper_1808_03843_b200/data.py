@@ -17,6 +17,8 @@ training loop keeps resident in HBM.
 
 from __future__ import annotations
 
+import math
+import struct
 from dataclasses import dataclass
 from typing import Iterable, NamedTuple
 
@@ -24,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .errors import DataError
+from .errors import DataError, FormatError, ParseError
 from .factors import predict_pairs
 
 
@@ -210,6 +212,110 @@ def build_device(triples, m: int | None = None, n: int | None = None) -> DeviceR
 def build(triples, m: int | None = None, n: int | None = None) -> SparseRatings:
     """Reference-compatible ``build``: device construction, host arrays back."""
     return build_device(triples, m, n).to_host()
+
+
+# ------------------------------------------------------------- text / cache I/O
+# File formats of the reference (data.py:1-26): text COO "user<d>item<d>rating"
+# per line (tab or comma, '#' comments and blank lines skipped), and the
+# little-endian binary CMFR cache (magic, u32 version, u64 m, n, nnz, then
+# row_ptr u64[m+1], col_idx u32[nnz], csr_val f32[nnz], col_ptr u64[n+1],
+# row_idx u32[nnz], csc_val f32[nnz]).  Files written by either package load
+# in the other.
+
+CACHE_MAGIC = b"CMFR"
+CACHE_VERSION = 1
+_DELIMS = {"tsv": "\t", "csv": ","}
+_HEADER = struct.Struct("<IQQQ")
+
+
+def parse_coo(lines, fmt: str = "tsv", m: int | None = None, n: int | None = None):
+    """Text triples -> (Triples, m, n); m, n default to max index + 1
+    (data.py:142-190).  Malformed lines raise ParseError with the 1-based line."""
+    if fmt not in _DELIMS:
+        raise DataError(f"unknown format {fmt!r}; expected 'tsv' or 'csv'")
+    delim = _DELIMS[fmt]
+    us, vs, rs = [], [], []
+    for line_no, raw in enumerate(lines, 1):
+        text = raw.strip()
+        if not text or text[0] == "#":
+            continue
+        fields = text.split(delim)
+        if len(fields) != 3:
+            raise ParseError(f"expected 3 fields separated by {delim!r}, got {len(fields)}", line_no)
+        try:
+            u, v, r = int(fields[0]), int(fields[1]), float(fields[2])
+        except ValueError as exc:
+            raise ParseError(str(exc), line_no) from None
+        if not math.isfinite(r):
+            raise ParseError(f"non-finite rating {fields[2]!r}", line_no)
+        if u < 0 or v < 0:
+            raise ParseError(f"negative index ({u}, {v})", line_no)
+        us.append(u)
+        vs.append(v)
+        rs.append(r)
+    t = Triples(np.array(us, dtype=np.int64), np.array(vs, dtype=np.int64),
+                np.array(rs, dtype=np.float64).astype(np.float32))
+    if m is None:
+        m = int(t.user.max()) + 1 if len(t) else 0
+    if n is None:
+        n = int(t.item.max()) + 1 if len(t) else 0
+    return t, m, n
+
+
+def load_coo(path, fmt: str = "tsv", m=None, n=None):
+    with open(path, "r", encoding="utf-8") as fh:
+        return parse_coo(fh, fmt=fmt, m=m, n=n)
+
+
+def save_coo(path, triples: Triples, fmt: str = "tsv") -> None:
+    """One line per triple, ratings with 9 significant digits (round-trips f32)."""
+    if fmt not in _DELIMS:
+        raise DataError(f"unknown format {fmt!r}; expected 'tsv' or 'csv'")
+    d = _DELIMS[fmt]
+    u, v, r = (np.asarray(a) for a in (triples.user, triples.item, triples.rating))
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.writelines(f"{a}{d}{b}{d}{c:.9g}\n" for a, b, c in zip(u.tolist(), v.tolist(), r.tolist()))
+
+
+_CACHE_LAYOUT = (("row_ptr", "<u8", np.int64), ("col_idx", "<u4", np.int32), ("csr_val", "<f4", np.float32),
+                 ("col_ptr", "<u8", np.int64), ("row_idx", "<u4", np.int32), ("csc_val", "<f4", np.float32))
+
+
+def save_cache(path, sr) -> None:
+    """Write the CMFR cache (data.py:305-314); a DeviceRatings is copied to the host."""
+    sr = sr.to_host() if isinstance(sr, DeviceRatings) else sr
+    with open(path, "wb") as fh:
+        fh.write(CACHE_MAGIC)
+        fh.write(_HEADER.pack(CACHE_VERSION, sr.m, sr.n, sr.nnz))
+        for name, disk, _ in _CACHE_LAYOUT:
+            fh.write(np.ascontiguousarray(getattr(sr, name), dtype=disk).tobytes())
+
+
+def load_cache(path) -> SparseRatings:
+    """Read a CMFR cache (data.py:317-345): bad magic, version, truncation or
+    trailing bytes raise FormatError."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if blob[:4] != CACHE_MAGIC:
+        raise FormatError(f"{path}: not a ratings cache (bad magic {blob[:4]!r})")
+    if len(blob) < 4 + _HEADER.size:
+        raise FormatError(f"{path}: truncated header")
+    version, m, n, nnz = _HEADER.unpack_from(blob, 4)
+    if version != CACHE_VERSION:
+        raise FormatError(f"{path}: unsupported cache version {version}")
+    counts = {"row_ptr": m + 1, "col_ptr": n + 1}
+    off = 4 + _HEADER.size
+    arrays = {}
+    for name, disk, mem in _CACHE_LAYOUT:
+        k = counts.get(name, nnz)
+        nb = k * np.dtype(disk).itemsize
+        if off + nb > len(blob):
+            raise FormatError(f"{path}: truncated payload")
+        arrays[name] = np.frombuffer(blob, dtype=disk, count=k, offset=off).astype(mem)
+        off += nb
+    if off != len(blob):
+        raise FormatError(f"{path}: trailing bytes after payload")
+    return SparseRatings(int(m), int(n), int(nnz), **arrays)
 
 
 # --------------------------------------------------------- split / synthesis

@@ -22,6 +22,9 @@ Fixtures:
                     non-negative instance: X, Theta, objectives and preference
                     RMSE per epoch (exact, cg-fp32), one
                     implicit_update_side and precompute_gram, mean percentile rank
+  io_cases.npz      file formats: the bytes of the reference's save_cache (CMFR)
+                    and save_coo (tsv, csv) for a small instance with duplicates,
+                    and its parse_coo of a text with comments / blank lines
   train_ml1m.npz    MovieLens-1M-shaped protocol (BASELINE configs[0]): RMSE and
                     objective per epoch for exact / cg-fp32 / cg-fp16, sampled
                     factor rows per epoch (exact), and SHA-256 digests of the
@@ -328,12 +331,37 @@ def implicit_small(cmf):
     np.savez_compressed(os.path.join(OUT, "implicit_small.npz"), **out)
 
 
+def io_cases(cmf):
+    out = {}
+    rng = np.random.default_rng(21)
+    m, n, k = 30, 20, 150
+    u = rng.integers(0, m, k).astype(np.int64)
+    v = rng.integers(0, n, k).astype(np.int64)
+    r = (rng.standard_normal(k) * 2).astype(np.float32)
+    t = cmf.Triples(u, v, r)
+    sr = cmf.build(t, m, n)
+    d = tempfile.mkdtemp()
+    cmf.data.save_cache(os.path.join(d, "c.cmfr"), sr)
+    out["u"], out["v"], out["r"], out["dims"] = u, v, r, np.array([m, n])
+    out["cache_bytes"] = np.frombuffer(open(os.path.join(d, "c.cmfr"), "rb").read(), dtype=np.uint8)
+    for fmt in ("tsv", "csv"):
+        cmf.data.save_coo(os.path.join(d, "c." + fmt), t, fmt=fmt)
+        out[fmt + "_bytes"] = np.frombuffer(open(os.path.join(d, "c." + fmt), "rb").read(), dtype=np.uint8)
+    text = "# header\n\n3\t4\t1.5\n  0\t0\t-2.25e-3 \n# mid\n7\t1\t3\n3\t4\t0.1\n"
+    pt, pm, pn = cmf.data.parse_coo(text.splitlines(True), fmt="tsv")
+    out["parse_text"] = np.frombuffer(text.encode(), dtype=np.uint8)
+    out["parse_u"], out["parse_v"], out["parse_r"] = pt.user, pt.item, pt.rating
+    out["parse_dims"] = np.array([pm, pn])
+    shutil.rmtree(d)
+    np.savez_compressed(os.path.join(OUT, "io_cases.npz"), **out)
+
+
 if __name__ == "__main__":
     cmf = import_reference()
     cmf.set_workers(os.cpu_count() or 1)
-    which = sys.argv[1:] or ["gram", "solve", "build", "data", "small", "implicit", "ml1m"]
+    which = sys.argv[1:] or ["gram", "solve", "build", "data", "small", "implicit", "io", "ml1m"]
     for w in which:
         {"gram": gram_cases, "solve": solve_cases, "build": build_cases,
          "data": data_cases, "small": train_small, "implicit": implicit_small,
-         "ml1m": train_ml1m}[w](cmf)
+         "io": io_cases, "ml1m": train_ml1m}[w](cmf)
         print("wrote", w)
