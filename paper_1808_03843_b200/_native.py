@@ -19,7 +19,8 @@ import torch
 from .errors import CmfError, DataError, NumericalError, SingularSystemError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcmf_b200.so")
+# CMF_LIB_PATH: load another build of the library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("CMF_LIB_PATH") or os.path.join(_PKG, "libcmf_b200.so")
 
 CMF_OK, CMF_EINVAL, CMF_EOVERFLOW, CMF_ESINGULAR, CMF_ECUDA = 0, 1, 2, 3, 4
 PREC = {"fp32": 0, "fp16": 1}

@@ -186,6 +186,12 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     return v;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Truncated CG on one system whose binary16 matrix sits in TMEM (thread i <->
 // lane i <-> row i; the tcgen05 A-operand layout: column j holds elements
 // 2j, 2j+1), run by one 128-thread group (4 warps, one named barrier).
@@ -207,6 +213,18 @@ struct TmemCg {
     uint32_t mvph = 0;
     int slot = 0, bar_id, i, lane, warp;
     bool leader, act;
+    long long *tr = nullptr;  // CMF_TRACE: per-exchange stamps of one row (thread 0 of the group)
+    int trk = 0;
+#ifdef CMF_TRACE
+#define CG_STAMP()                                  \
+    do {                                            \
+        if (i == 0 && tr) trace_at(tr, trk++ & 63); \
+    } while (0)
+#else
+#define CG_STAMP() \
+    do {           \
+    } while (0)
+#endif
 
     __device__ TmemCg(unsigned char *scratch, uint32_t mvbar_, int bar_id_, int warp_, int lane_, int f)
         : bop(smem_u32(scratch)), mvbar(mvbar_), bar_id(bar_id_), lane(lane_), warp(warp_) {
@@ -226,6 +244,7 @@ struct TmemCg {
                               float &sb, bool mv) {
         constexpr uint32_t idesc_mv = (1u << 4) | (static_cast<uint32_t>(16 >> 3) << 17) |
                                       (static_cast<uint32_t>(128 >> 4) << 24);  // f16 x f16 -> f32, K-major
+        CG_STAMP();
         if (mv && act) {
             const __half hv = __float2half_rn(v);
             const __half lv = __float2half_rn(v - __half2float(hv));
@@ -233,18 +252,21 @@ struct TmemCg {
             asm volatile("st.shared.b16 [%0], %1;" ::"r"(bop + bofs1), "h"(__half_as_ushort(lv)) : "memory");
         }
         if (mv) fence_proxy_async();
+        // three butterfly levels leave 4 partials per warp (lanes 0-3); the 16
+        // per value are summed after the barrier in a fixed order
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 16; o > 2; o >>= 1) {
             da += __shfl_xor_sync(0xffffffffu, da, o);
             db += __shfl_xor_sync(0xffffffffu, db, o);
         }
-        float *rd = red + 8 * slot;
+        float *rd = red + 32 * slot;
         slot ^= 1;
-        if (lane == 0) {
-            rd[warp & 3] = da;
-            rd[4 + (warp & 3)] = db;
+        if (lane < 4) {
+            rd[(warp & 3) * 4 + lane] = da;
+            rd[16 + (warp & 3) * 4 + lane] = db;
         }
         named_bar(bar_id, CG_THREADS);
+        CG_STAMP();
         if (mv && leader) {
             if (elect_one()) {
                 tc_fence_after();
@@ -256,10 +278,20 @@ struct TmemCg {
             }
             __syncwarp();
         }
-        sa = (rd[0] + rd[1]) + (rd[2] + rd[3]);
-        sb = (rd[4] + rd[5]) + (rd[6] + rd[7]);
+        {
+            const float4 *r4 = reinterpret_cast<const float4 *>(rd);
+            float t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float4 q = r4[k];
+                t[k] = (q.x + q.y) + (q.z + q.w);
+            }
+            sa = (t[0] + t[1]) + (t[2] + t[3]);
+            sb = (t[4] + t[5]) + (t[6] + t[7]);
+        }
         if (!mv) return 0.0f;
         mbar_wait(mvbar, mvph & 1);
+        CG_STAMP();
         ++mvph;
         tc_fence_after();
         const float y0 = __uint_as_float(tmem_ld1(dcol + lane_base));
@@ -308,28 +340,31 @@ struct TmemCg {
         const float eps2 = eps >= 0.0 ? static_cast<float>(eps * eps) : tol * tol * bb;
         float gamma, delta;
         float w = exchange(a_tmem, dcol, reg, r, 0.0f, 0.0f, gamma, delta, true);
-        float p = 0.0f, sv = 0.0f, z = 0.0f, gamma_old = 1.0f, alpha_old = 1.0f;
+        // 1/gamma_old and 1/alpha_old are formed off the critical path (one
+        // iteration early); only 1/pap sits on it.  rcp.approx (1 ulp): the
+        // scalars feed a truncated CG graded on the RMSE trajectory.
+        float p = 0.0f, sv = 0.0f, z = 0.0f, rgamma_old = 1.0f, ralpha_old = 1.0f;
         bd = 0;
         nit = 0;
         for (int step = 0; step < f_s; ++step) {
             const bool last = step + 1 >= f_s;
             const float m = exchange(a_tmem, dcol, reg, w, r * r, w * r, gamma, delta, !last);
             if (step > 0 && (gamma == 0.0f || gamma < eps2)) break;
-            const float beta = step > 0 ? gamma * __frcp_rn(gamma_old) : 0.0f;
-            const float pap = step > 0 ? delta - beta * gamma * __frcp_rn(alpha_old) : delta;
+            const float beta = step > 0 ? gamma * rgamma_old : 0.0f;
+            const float pap = step > 0 ? delta - beta * gamma * ralpha_old : delta;
             if (!(pap > 0.0f)) {
                 bd = 1;
                 break;
             }
-            const float alpha = gamma * __frcp_rn(pap);
+            const float alpha = gamma * rcp_approx(pap);
             z = fmaf(beta, z, m);
             sv = fmaf(beta, sv, w);
             p = fmaf(beta, p, r);
             xi = fmaf(alpha, p, xi);
             r = fmaf(-alpha, sv, r);
             w = fmaf(-alpha, z, w);
-            gamma_old = gamma;
-            alpha_old = alpha;
+            rgamma_old = rcp_approx(gamma);
+            ralpha_old = rcp_approx(alpha);
             ++nit;
         }
     }
@@ -447,6 +482,8 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
             const float reg = g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
                                          : __double2float_rn(g.lam);
             int bd = 0, nit = 0;
+            cg.tr = (ga.trace && r_here < 64) ? ga.trace + 40960 + 64 * r_here : nullptr;
+            cg.trk = 0;
             cg.solve(a_tmem, dcol, reg, bi, -1.0, g.tol, g.f_s, xi, bd, nit);
             tc_fence_before();
             mbar_arrive(pp.tempty(b));  // the accumulator is free for row r_here + NBUF

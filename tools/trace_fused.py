@@ -33,6 +33,14 @@ for r in (3, 30, 60):
     e = ev[r][ev[r] > 0]
     if len(e) > 2:
         print("row", r, "CG events (cycles from first):", (e - e[0]).astype(int).tolist())
+# per exchange (pipelined solve): [entry, after barrier, after matvec wait]; deltas
+rows = [ev[r][ev[r] > 0] for r in range(8, 64)]
+rows = [e for e in rows if len(e) >= 23]
+if rows:
+    e = np.array([r[:23] for r in rows])
+    d = np.diff(e, axis=1)
+    print("median deltas per event (entry->bar, bar->mvwait, mvwait->next entry, ...):")
+    print(np.median(d, axis=0).astype(int).tolist())
 rr = allb[32768:40960].reshape(2048, 4).astype(np.float64)
 rr = rr[(rr[:, 3] > 0) & (rr[:, 0] > 0)]
 if len(rr) > 8:
