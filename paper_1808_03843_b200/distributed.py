@@ -61,6 +61,13 @@ class RowGather:
 
     def __call__(self, full: torch.Tensor, rank: int, group=None):
         import torch.distributed as dist
+        if full.is_cuda and dist.get_backend(group) == "gloo":
+            # gloo has no CUDA all-gather: stage through host memory (multi-rank
+            # tests on one device; production runs NCCL over NVLink)
+            host = full.cpu()
+            RowGather(self.bounds, full.shape[1], torch.device("cpu"), full.dtype)(host, rank, group)
+            full.copy_(host)
+            return
         lo, hi = self.bounds[rank], self.bounds[rank + 1]
         if self.equal and full.is_contiguous():
             dist.all_gather_into_tensor(full[: self.world * self.maxrows].view(-1),
