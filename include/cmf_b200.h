@@ -119,10 +119,12 @@ int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi1
  * solved in place, target[u] <- CG_{f_s}(A_u + reg*I, b_u, x0 = target[u]),
  * eps = cg_tol * ||b_u||.  A_u never reaches HBM.  Replaces als.update_side
  * (als.py:54-74) for SolverConfig(method="cg").  f <= 120.  *breakdowns
- * (device int, nullable) accumulates p^T A p <= 0 exits.
+ * (device int, nullable) accumulates p^T A p <= 0 exits.  nnz =
+ * indptr[nrows] - indptr[0], counted on the host: rows averaging >= 1024
+ * ratings (the item side) run a CTA shape with fewer CG warps.
  */
 int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
-                        int64_t nrows, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
+                        int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
                         int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
                         int32_t *breakdowns, void *stream);
 /* Debugging aid: a device buffer of 8 * 4096 int64 (or NULL to switch off) that

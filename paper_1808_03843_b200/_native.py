@@ -41,7 +41,7 @@ _SIGNATURES = {
                                                  _vp, _vp]),
     "cmf_tc_width": (ctypes.c_int, [_i32]),
     "cmf_debug_trace": (ctypes.c_int, [_vp]),
-    "cmf_fused_cg_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
+    "cmf_fused_cg_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
                                            _i32, _f64, _vp, _vp]),
     "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
     "cmf_spmm_bias": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),

@@ -171,9 +171,12 @@ class HalfUpdatePlan:
         return self.shadow, None
 
     def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
-               row0: int = 0, nrows: int | None = None, reuse_shadow: bool = False):
+               row0: int = 0, nrows: int | None = None, reuse_shadow: bool = False,
+               nnz: int | None = None):
         """Gram(+bias) -> solve for rows [row0, row0+nrows) of the view, block by
-        block, solutions written into tg (rows indexed like the view)."""
+        block, solutions written into tg (rows indexed like the view).  ``nnz``:
+        ratings in those rows (default: all of the view's), which picks the
+        fused kernel's CTA shape."""
         f, solver = self.f, self.solver
         nrows = self.nrows if nrows is None else nrows
         st = nat.stream_ptr()
@@ -195,8 +198,9 @@ class HalfUpdatePlan:
             if record is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
+            nnz = int(values.numel()) if nnz is None else int(nnz)
             nat.call("cmf_fused_cg_update", nat.ptr(indptr) + 8 * row0, nat.ptr(indices),
-                     nat.ptr(values), nrows, nat.ptr(shadow), fx.shape[0], self.w16, f, float(lam),
+                     nat.ptr(values), nrows, nnz, nat.ptr(shadow), fx.shape[0], self.w16, f, float(lam),
                      int(bool(weighted_reg)), nat.ptr(tg) + 4 * row0 * f, int(solver.cg_iters),
                      float(solver.cg_tol), nat.ptr(self.flags) + 4, st)
             if record is not None:
@@ -355,7 +359,8 @@ def _update_side_streamed(view: RowView, fixed, target, lam, solver, weighted_re
     for ci, (r0, r1) in enumerate(zip(bounds[:-1], bounds[1:])):
         comp.wait_event(evs[ci])
         plan.launch(indptr, indices, values, fx, tg, lam, weighted_reg, "tc", rec,
-                    row0=int(r0), nrows=int(r1 - r0), reuse_shadow=ci > 0)
+                    row0=int(r0), nrows=int(r1 - r0), reuse_shadow=ci > 0,
+                    nnz=int(ptr_np[r1] - ptr_np[r0]))
         done = torch.cuda.Event()
         done.record(comp)
         d2h.wait_event(done)

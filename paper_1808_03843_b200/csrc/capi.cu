@@ -26,7 +26,7 @@ int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, con
 int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, int, float, int32_t *, cudaStream_t);
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
-                    int, float *, int, double, int32_t *, cudaStream_t);
+                    int, float *, int64_t, int, double, int32_t *, cudaStream_t);
 int factors_to_half_launch(const float *, int64_t, int, void *, int, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
                      float *, cudaStream_t);
@@ -146,7 +146,7 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
 }
 
 int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
-                        int64_t nrows, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
+                        int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
                         int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
                         int32_t *breakdowns, void *stream) {
     REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
@@ -155,8 +155,8 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
     if (nrows == 0) return CMF_OK;
     REQUIRE(indptr && fixed16 && target, "null argument");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
-    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, f_s,
-                           cg_tol, breakdowns, S(stream));
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, nnz,
+                           f_s, cg_tol, breakdowns, S(stream));
 }
 
 int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,

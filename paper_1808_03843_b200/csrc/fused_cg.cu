@@ -46,9 +46,13 @@ constexpr int MVB_BYTES = 5120;    // + warp partials, 1024-aligned per group
 // setmaxnreg: the CG warpgroups hold a register row of A_u (4*FC floats) and
 // grow to CG_REGS, the auxiliary warpgroups shrink to AUX_REGS, so that
 // NG*128*CG_REGS + 256*AUX_REGS == THREADS*LAUNCH_REGS <= 64K registers.
-template <int FC>
+// LONG: rows averaging >= LONG_ROW_NNZ ratings (the item side): the gather
+// dominates and CG is rare, and two CG groups leave the producers more of the
+// SM (measured: Theta side 3.21 -> 3.03 ms at Netflix shape).
+constexpr int LONG_ROW_NNZ = 1024;
+template <int FC, bool LONG = false>
 struct FusedShape {
-    static constexpr int NG = FC <= 26 ? 3 : 2;
+    static constexpr int NG = (FC <= 26 && !LONG) ? 3 : 2;
     static constexpr int NBUF = NG + 1;  // TMEM accumulators rotate over the NG groups
     static constexpr int THREADS = 32 * (4 * NG + F_PROD + 1);
     static constexpr int MMA_WARP = 4 * NG + F_PROD;
@@ -371,12 +375,14 @@ struct TmemCg {
 };
 
 // FC = ceil(f/4): register row of A_u as FC*2 float2 pairs.
-template <int FC>
-__global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(const __grid_constant__ FusedArgs g) {
-    constexpr int F_GROUPS = FusedShape<FC>::NG;
-    constexpr int F_THREADS = FusedShape<FC>::THREADS;
-    constexpr int F_MMA_WARP = FusedShape<FC>::MMA_WARP;
-    constexpr int NBUF = FusedShape<FC>::NBUF;
+template <int FC, bool LONG>
+__global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
+    fused_cg_kernel(const __grid_constant__ FusedArgs g) {
+    using Shape = FusedShape<FC, LONG>;
+    constexpr int F_GROUPS = Shape::NG;
+    constexpr int F_THREADS = Shape::THREADS;
+    constexpr int F_MMA_WARP = Shape::MMA_WARP;
+    constexpr int NBUF = Shape::NBUF;
     using PipeT = FPipe<NBUF>;
     constexpr int KP = (FC * 4 + 15) / 16 * 16;  // matvec K extent (>= f), 16-half MMA steps
     constexpr int F_STAGES = PipeT::kStages;
@@ -409,12 +415,12 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
     const int64_t G = gridDim.x;
 
     if (warp >= 4 * F_GROUPS && warp < F_MMA_WARP) {
-        regs_dec<FusedShape<FC>::AUX_REGS>();
+        regs_dec<Shape::AUX_REGS>();
         if (warp - 4 * F_GROUPS < g.nprod && !g.cg_only)
             produce<F_STAGES, false, NBUF>(ga, g.fixed16, nullptr, g.W, pp, warp - 4 * F_GROUPS, g.nprod, lane,
                                            blockIdx.x, G);
     } else if (warp == F_MMA_WARP) {
-        regs_dec<FusedShape<FC>::AUX_REGS>();
+        regs_dec<Shape::AUX_REGS>();
         if (!g.cg_only) {
             issue_mma<F_STAGES, false, NBUF>(ga, pp, tmem_base, g.N, blockIdx.x, G);
         } else {  // timing experiment: hand out the (stale) accumulators without any MMA
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(FusedShape<FC>::THREADS, 1) fused_cg_kernel(co
             }
         }
     } else {
-        regs_inc<FusedShape<FC>::CG_REGS>();
+        regs_inc<Shape::CG_REGS>();
         // ------------------------------------------------------------ CG groups
         const int grp = warp >> 2;             // rows r with r % NG == grp
         const int i = (warp & 3) * 32 + lane;  // row of A_u == TMEM lane
@@ -638,9 +644,9 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
 int gram_tc_width(int f);
 int fused_cg_trace(void *buf) { return tc::set_trace_buf(buf); }
 
-template <int FC>
+template <int FC, bool LONG>
 static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
-    using Shape = tc::FusedShape<FC>;
+    using Shape = tc::FusedShape<FC, LONG>;
     using PipeT = tc::FPipe<Shape::NBUF>;
     const size_t smem = 1024 + PipeT::kStages * PipeT::kStageBytes + Shape::NG * tc::MVB_BYTES +
                         (PipeT::kBars + Shape::NG) * 8 + 16;
@@ -651,7 +657,7 @@ static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
     g.dmv_off = (KP / 2 + 15) / 16 * 16;
     if (!g.dmv_tail && g.dmv_off + 16 > g.N) return set_error(CMF_EINVAL, "fused CG: no TMEM room for f=%d", g.gather.f);
     g.tmem_cols = 512;
-    auto k = tc::fused_cg_kernel<FC>;
+    auto k = tc::fused_cg_kernel<FC, LONG>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return set_error(CMF_ECUDA, "fused_cg smem attr: %s", cudaGetErrorString(e));
     int dev = 0, sms = 148;
@@ -665,12 +671,14 @@ static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
 
 // f (<= 120) -> template instance FC = ceil(f/4), bucketed
 #define CMF_FUSED_CASE(FMAX, FCV) \
-    if (f <= FMAX) return launch_fused<FCV>(g, st);
+    if (f <= FMAX) return long_rows ? launch_fused<FCV, true>(g, st) : launch_fused<FCV, false>(g, st);
 
 int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
                     const void *fixed16, int64_t ncols, int W, int f, double lam, int weighted, float *target,
-                    int f_s, double cg_tol, int32_t *breakdowns, cudaStream_t st) {
+                    int64_t nnz, int f_s, double cg_tol, int32_t *breakdowns, cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
+    if (nnz < 0) return set_error(CMF_EINVAL, "negative rating count");
+    const bool long_rows = nnz >= tc::LONG_ROW_NNZ * nrows;
     if (W + 2 > tc::M) return set_error(CMF_EINVAL, "fused CG supports f <= %d (got %d)", tc::M - 8, f);
     if (W != gram_tc_width(f)) return set_error(CMF_EINVAL, "fixed16 width must be %d", gram_tc_width(f));
     if ((reinterpret_cast<uintptr_t>(fixed16) & 15) != 0) return set_error(CMF_EINVAL, "fixed16 must be 16-byte aligned");
