@@ -80,7 +80,7 @@ struct FusedArgs {
     int weighted;
     float *target;  // (nrows, f) in/out
     int f_s;
-    int nprod;  // active producer warps (<= F_PROD)
+    int nprod;  // active producer warps (<= F_PROD; the others exit at once)
     int cg_only;  // timing experiment (CMF_FUSED_CG_ONLY): no gather / MMA
     float tol;
     int32_t *breakdowns;
@@ -700,8 +700,15 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
     g.f_s = f_s;
     {
         const char *e = getenv("CMF_FUSED_PROD");
-        g.nprod = e ? atoi(e) : tc::F_PROD;
-        if (g.nprod < 1 || g.nprod > tc::F_PROD) g.nprod = tc::F_PROD;
+        // Short rows over an L2-resident fixed side (Netflix users: 3.7 MB of
+        // item factors) gather fast enough with 5 warps, and the 2 idle ones
+        // leave issue slots to the CG groups (update-X 5.60 -> 5.22 ms); when
+        // the gather misses L2 (a large fixed side, or long rows) all 7 pay off
+        // (Yahoo: 17.8 vs 18.3 ms with 5).  Same-box A/B, tools/ab_probe.sh.
+        const bool l2_resident = static_cast<int64_t>(ncols) * W * 2 <= (int64_t(32) << 20);
+        const int dflt = (!long_rows && l2_resident) ? 5 : tc::F_PROD;
+        g.nprod = e ? atoi(e) : dflt;
+        if (g.nprod < 1 || g.nprod > tc::F_PROD) g.nprod = dflt;
         const char *c = getenv("CMF_FUSED_CG_ONLY");
         g.cg_only = c ? atoi(c) : 0;
     }

@@ -16,7 +16,7 @@ import paper_1808_03843_b200 as cmfb  # noqa: E402
 from paper_1808_03843_b200.als import HalfUpdatePlan, resolve_events  # noqa: E402
 
 SHAPES = {"netflix": (480_189, 17_770, 99_000_000), "ml1m": (6_040, 3_706, 1_000_000),
-          "small": (48_019, 17_770, 9_900_000)}
+          "small": (48_019, 17_770, 9_900_000), "yahoo": (1_000_990, 624_961, 252_800_000)}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="netflix")
