@@ -237,7 +237,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.shape}-f{f}-{args.solver}", "m": m, "n": n, "nnz": nnz,
+        "config": {"workload": workload_label(args.shape, f, args.solver, world), "m": m, "n": n, "nnz": nnz,
                    "f": f, "solver": args.solver, "parallelism": "host-cpu"},
         "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
                          "sample": sample},
