@@ -10,8 +10,10 @@
 // threads stride over that suffix with no idle work:
 //   TRSM:   rows of panel p below the diagonal, L_Ip = A_Ip L_pp^-T (one row
 //           per thread), and the forward-substitution block y_p = L_pp^-1 z_p
-//   update: A_IJ -= L_Ip L_Jp^T over the active tiles (4+4+4 LDS.128, 32
-//           FFMA2, 4 STS.128 each), z_I -= L_Ip y_p, and the owner of the next
+//   update: A_IJ -= L_Ip L_Jp^T over the active tiles (rows of L_Ip, columns
+//           of L_Jp from a transposed copy of the panel so that FFMA2 pairs
+//           come straight from float4 loads: 12 LDS.128, 32 FFMA2, 4 STS.128
+//           per tile), z_I -= L_Ip y_p, and the owner of the next
 //           diagonal tile factorises it right after updating it (look-ahead).
 // Two barriers per 4-column panel.  The backward solve L^T x = y runs on warp
 // 0 (lanes own rows l + 32q, shuffles, no block barriers).  Padding rows
@@ -70,13 +72,14 @@ __global__ void __launch_bounds__(128, 8) chol_smem_kernel(const float *A, int64
     constexpr int NT = 128;
     const int tid = threadIdx.x;
     const int fp = (f + 3) & ~3, TR = fp >> 2, T = TR * (TR + 1) / 2;
-    // shared: tiles | z / y (fp) | 1/L_ii (fp) | tile rows I, cols J (T bytes each) | flag.
+    // shared: tiles | z / y (fp) | 1/L_ii (fp) | panel^T (4 fp) | tile rows I, cols J | flag.
     // Row x of tile t is the float4 tiles[x * T + t]: threads working on
     // consecutive tiles touch consecutive float4s (no bank conflicts).
     float4 *tiles = reinterpret_cast<float4 *>(csm);
     float *zy = csm + 16 * T;
     float *rdiag = zy + fp;
-    unsigned char *tI = reinterpret_cast<unsigned char *>(rdiag + fp);
+    float *pt = rdiag + fp;  // panel p transposed: pt[c * fp + r] = L[r][4p + c]
+    unsigned char *tI = reinterpret_cast<unsigned char *>(pt + 4 * fp);
     const int T4 = (T + 3) & ~3;
     unsigned char *tJ = tI + T4;
     int *flag = reinterpret_cast<int *>(tJ + T4);
@@ -99,28 +102,30 @@ __global__ void __launch_bounds__(128, 8) chol_smem_kernel(const float *A, int64
         const int i = f + tid;
         csm[4 * ((i & 3) * T + col_start(i >> 2, TR)) + (i & 3)] = 1.0f;
     }
-    // scatter the packed lower triangle (row-major, i(i+1)/2 + j): 8 loads in flight per thread
+    // scatter the packed lower triangle (row-major, k = i(i+1)/2 + j), 14 loads
+    // in flight per thread; row of k from an approximate square root + fix-up
     {
         const float *src = A + s * a_stride;
-        const int64_t P = packed_size(f);
-        for (int64_t k0 = tid; k0 < P; k0 += 8 * NT) {
-            float v[8];
-            int off[8];
+        const int P = static_cast<int>(packed_size(f));
+        for (int k0 = tid; k0 < P; k0 += 14 * NT) {
+            float v[14];
+            int off[14];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int64_t k = k0 + u * NT;
+            for (int u = 0; u < 14; ++u) {
+                const int k = k0 + u * NT;
                 off[u] = -1;
                 if (k < P) {
-                    int i = static_cast<int>((sqrtf(8.0f * static_cast<float>(k) + 1.0f) - 1.0f) * 0.5f);
-                    while (static_cast<int64_t>(i + 1) * (i + 2) / 2 <= k) ++i;
-                    while (static_cast<int64_t>(i) * (i + 1) / 2 > k) --i;
-                    const int j = static_cast<int>(k - static_cast<int64_t>(i) * (i + 1) / 2);
+                    const float q = 8.0f * static_cast<float>(k) + 1.0f;
+                    int i = static_cast<int>((q * rsqrtf(q) - 1.0f) * 0.5f);
+                    if ((i + 1) * (i + 2) / 2 <= k) ++i;
+                    if (i * (i + 1) / 2 > k) --i;
+                    const int j = k - i * (i + 1) / 2;
                     v[u] = __ldg(src + k);
                     off[u] = 4 * ((i & 3) * T + col_start(j >> 2, TR) + (i >> 2) - (j >> 2)) + (j & 3);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < 14; ++u)
                 if (off[u] >= 0) csm[off[u]] = v[u];
         }
     }
@@ -149,6 +154,10 @@ __global__ void __launch_bounds__(128, 8) chol_smem_kernel(const float *A, int64
             const float y2 = fmaf(-y1, l2.y, fmaf(-y0, l2.x, a.z)) * rdiag[4 * p + 2];
             const float y3 = fmaf(-y2, l3.z, fmaf(-y1, l3.y, fmaf(-y0, l3.x, a.w))) * rdiag[4 * p + 3];
             *row = make_float4(y0, y1, y2, y3);
+            pt[r] = y0;
+            pt[fp + r] = y1;
+            pt[2 * fp + r] = y2;
+            pt[3 * fp + r] = y3;
         }
         if (tid == NT - 1) {
             const float4 l1 = Lpp[T], l2 = Lpp[2 * T], l3 = Lpp[3 * T];
@@ -165,31 +174,29 @@ __global__ void __launch_bounds__(128, 8) chol_smem_kernel(const float *A, int64
         __syncthreads();
         if (p + 1 == TR) break;
         // (2) trailing update over the active suffix; z_I -= L_Ip y_p
+        // thread 0 takes only the next diagonal tile (it factorises it right
+        // after the update); threads 1..NT-1 share the rest
         const int start = col_start(p + 1, TR);
-        for (int t = start + tid; t < T; t += NT) {
+        const int tstep = tid == 0 ? T : NT - 1;
+        for (int t = start + tid; t < T; t += tstep) {
             const int I = tI[t], J = tJ[t];
             const float4 *LI = tiles + cp + I - p;
-            const float4 *LJ = tiles + cp + J - p;
+            // columns c of L_Jp (rows 4J..4J+3) from the transposed panel
             float4 lj[4];
 #pragma unroll
-            for (int y = 0; y < 4; ++y) lj[y] = LJ[y * T];
+            for (int c = 0; c < 4; ++c) lj[c] = *reinterpret_cast<const float4 *>(pt + c * fp + 4 * J);
             float4 *at = tiles + t;
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
                 const float4 li = LI[x * T];
-                float4 a = at[x * T];
+                const float4 a = at[x * T];
                 float2 a01 = make_float2(a.x, a.y), a23 = make_float2(a.z, a.w);
-                // a[x][y] -= sum_c li[c] * lj[y][c]
                 const float lic[4] = {li.x, li.y, li.z, li.w};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < 4; ++c) {  // a[x][y] -= L[4I+x][c] * L[4J+y][c]
                     const float2 m = make_float2(-lic[c], -lic[c]);
-                    const float ljc[4] = {c == 0 ? lj[0].x : c == 1 ? lj[0].y : c == 2 ? lj[0].z : lj[0].w,
-                                          c == 0 ? lj[1].x : c == 1 ? lj[1].y : c == 2 ? lj[1].z : lj[1].w,
-                                          c == 0 ? lj[2].x : c == 1 ? lj[2].y : c == 2 ? lj[2].z : lj[2].w,
-                                          c == 0 ? lj[3].x : c == 1 ? lj[3].y : c == 2 ? lj[3].z : lj[3].w};
-                    a01 = __ffma2_rn(m, make_float2(ljc[0], ljc[1]), a01);
-                    a23 = __ffma2_rn(m, make_float2(ljc[2], ljc[3]), a23);
+                    a01 = __ffma2_rn(m, make_float2(lj[c].x, lj[c].y), a01);
+                    a23 = __ffma2_rn(m, make_float2(lj[c].z, lj[c].w), a23);
                 }
                 at[x * T] = make_float4(a01.x, a01.y, a23.x, a23.y);
             }
@@ -258,7 +265,7 @@ int chol_smem_launch(const float *a, int64_t a_stride, const float *b, const int
     if (nsys == 0) return CMF_OK;
     if (f > 128) return set_error(CMF_EINVAL, "f=%d too large for the tile Cholesky", f);
     const int fp = (f + 3) & ~3, TR = fp / 4, T = TR * (TR + 1) / 2;
-    const size_t smem = static_cast<size_t>(16 * T + 2 * fp) * sizeof(float) + 2 * ((T + 3) & ~3) + 16;
+    const size_t smem = static_cast<size_t>(16 * T + 6 * fp) * sizeof(float) + 2 * ((T + 3) & ~3) + 16;
     if (smem > 48 * 1024) {
         cudaError_t e =
             cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
