@@ -24,6 +24,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -78,11 +79,21 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+            # line-buffered so that terminate() loses no samples
+            cmd = ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                   "--format=csv,noheader,nounits", "-lms", "20"]
+            if shutil.which("stdbuf"):
+                cmd = ["stdbuf", "-oL"] + cmd
+            self.proc = subprocess.Popen(cmd, stdout=self.fh, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return self
+        # start the timed region only once sampling is running
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and self.proc.poll() is None:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *exc):
