@@ -81,7 +81,6 @@ struct FusedArgs {
     float *target;  // (nrows, f) in/out
     int f_s;
     int nprod;  // active producer warps (<= F_PROD; the others exit at once)
-    int cg_only;  // timing experiment (CMF_FUSED_CG_ONLY): no gather / MMA
     float tol;
     int32_t *breakdowns;
 };
@@ -416,24 +415,12 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
 
     if (warp >= 4 * F_GROUPS && warp < F_MMA_WARP) {
         regs_dec<Shape::AUX_REGS>();
-        if (warp - 4 * F_GROUPS < g.nprod && !g.cg_only)
+        if (warp - 4 * F_GROUPS < g.nprod)
             produce<F_STAGES, false, NBUF>(ga, g.fixed16, nullptr, g.W, pp, warp - 4 * F_GROUPS, g.nprod, lane,
                                            blockIdx.x, G);
     } else if (warp == F_MMA_WARP) {
         regs_dec<Shape::AUX_REGS>();
-        if (!g.cg_only) {
-            issue_mma<F_STAGES, false, NBUF>(ga, pp, tmem_base, g.N, blockIdx.x, G);
-        } else {  // timing experiment: hand out the (stale) accumulators without any MMA
-            uint32_t rowc = 0;
-            for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
-                if (ga.indptr[u + 1] == ga.indptr[u]) continue;
-                const int b = rowc % NBUF;
-                mbar_wait(pp.tempty(b), ((rowc / NBUF) & 1) ^ 1);
-                if (elect_one()) tc_commit(pp.tfull(b));
-                __syncwarp();
-                ++rowc;
-            }
-        }
+        issue_mma<F_STAGES, false, NBUF>(ga, pp, tmem_base, g.N, blockIdx.x, G);
     } else {
         regs_inc<Shape::CG_REGS>();
         // ------------------------------------------------------------ CG groups
@@ -709,8 +696,6 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
         const int dflt = (!long_rows && l2_resident) ? 5 : tc::F_PROD;
         g.nprod = e ? atoi(e) : dflt;
         if (g.nprod < 1 || g.nprod > tc::F_PROD) g.nprod = dflt;
-        const char *c = getenv("CMF_FUSED_CG_ONLY");
-        g.cg_only = c ? atoi(c) : 0;
     }
     g.tol = static_cast<float>(cg_tol);
     g.breakdowns = breakdowns;
