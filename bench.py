@@ -270,9 +270,17 @@ def main():
     from paper_1808_03843_b200 import distributed as cdist
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # CMF_DIST_BACKEND=gloo runs the multi-rank flow on a box with fewer GPUs than
+    # ranks (ranks share devices; RowGather stages through host memory) -- a
+    # functional check only; production runs NCCL, one GPU per rank
+    backend = os.environ.get("CMF_DIST_BACKEND", "nccl")
+    dev_index = local % torch.cuda.device_count() if backend == "gloo" else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     m, n, nnz = SHAPES[args.shape]
     f = args.f
     method, precision = SOLVERS[args.solver]
@@ -302,7 +310,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         # cudaProfilerStart/Stop bracket the timed region so that
         # `ncu --profile-from-start off` lists exactly the step's launches
         torch.cuda.profiler.start()
@@ -415,6 +423,10 @@ def main():
         torch.cuda.synchronize()
         kx = resolve_events(kx)
         ems = e0.elapsed_time(e1) / max(2, args.steps // 2)
+        if world > 1:
+            te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            ems = float(te.item())
         result["exact"] = {"workload": f"{args.shape}-f{f}-exact (BASELINE configs[1])",
                            "sec_per_iteration": ems / 1e3,
                            "gram_ms": sum(sum(v) for k, v in kx.items() if k.startswith("gram")) / max(2, args.steps // 2),
