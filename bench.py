@@ -303,6 +303,15 @@ def main():
 
     # ---- warm-up, then the timed region (K iterations, events on the launch stream)
     x, th = x0.clone(), th0.clone()
+    exchange = "none (single GPU)" if world == 1 else "NCCL all-gather after each half"
+    if world > 1 and os.environ.get("CMF_PEER_STORE", "1") != "0":
+        # the fused kernel stores solved rows into every rank's replica (CUDA IPC
+        # over NVLink) instead of an all-gather; any setup failure keeps NCCL
+        try:
+            if engine.attach_replicas(x, th):
+                exchange = "peer stores from the fused kernel (CUDA IPC / NVLink), rank barrier per half"
+        except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+            exchange = f"NCCL all-gather (peer-store setup failed: {exc})"
     run_steps(x, th, args.warmup)
     kern = {}
     nat.LAUNCHES[0] = 0
@@ -385,11 +394,13 @@ def main():
                    "m": m, "n": n, "nnz": train.nnz, "f": f, "lambda": 0.05,
                    "solver": args.solver, "cg_iters": 6, "gram_kernel": gram_kernel,
                    "parallelism": f"rows sharded x{world}" if world > 1 else "single-gpu",
+                   "exchange": exchange,
                    "l2": "inputs > L2 (ratings 1.6 GB + Gram workspace)"},
         "gpu_launches": launches,
         "phase_ms_per_step": {"gram": gram_ms / args.steps, "solve": solve_ms / args.steps,
                               "fused_gram_cg": fused_ms / args.steps,
-                              "allgather": per_kernel.get("allgather", {}).get("ms_total", 0.0)
+                              "allgather": per_kernel.get("allgather", {}).get("ms_total", 0.0) / args.steps,
+                              "peer_barrier": per_kernel.get("peer_barrier", {}).get("ms_total", 0.0)
                               / args.steps},
         "kernels": {"gram_tflops": gram_tflops, "solve_gbs": solve_gbs,
                     "solve_hbm_frac": solve_gbs / pk["hbm"], "fused_tflops": fused_tflops,

@@ -127,6 +127,25 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
                         int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
                         int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
                         int32_t *breakdowns, void *stream);
+/*
+ * Multi-GPU form of cmf_fused_cg_update: every solved row is also stored into
+ * npeers replicas of `target` (peer_targets: a DEVICE array of device
+ * pointers, e.g. CUDA-IPC mappings of the other ranks' factor matrices over
+ * NVLink, each offset like `target`), so the all-gather after the half-update
+ * disappears.  The caller orders the halves (stream sync + rank barrier).
+ * Replaces the update + NCCL all-gather of the sharded driver.
+ */
+int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, const float *values,
+                              int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
+                              int32_t f, double lam, int32_t weighted_reg, float *target,
+                              float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
+                              int32_t *breakdowns, void *stream);
+/* CUDA IPC for the peer replicas: export a device pointer (any address inside
+ * an allocation) as a 64-byte handle + offset; open it in another process
+ * (peer access enabled lazily over NVLink); close with the same offset. */
+int cmf_ipc_export(const void *ptr, void *handle64, int64_t *offset);
+int cmf_ipc_open(const void *handle64, int64_t offset, void **ptr_out);
+int cmf_ipc_close(void *ptr, int64_t offset);
 /* Debugging aid: a device buffer of 8 * 4096 int64 (or NULL to switch off) that
  * CTA 0 of the tensor-core kernels fills with clock64 stamps per operand stage
  * (producer wait / slot free / copies issued / MMA sees data / MMA commit). */

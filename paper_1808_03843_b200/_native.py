@@ -41,8 +41,13 @@ _SIGNATURES = {
                                                  _vp, _vp]),
     "cmf_tc_width": (ctypes.c_int, [_i32]),
     "cmf_debug_trace": (ctypes.c_int, [_vp]),
+    "cmf_ipc_export": (ctypes.c_int, [_vp, _vp, _vp]),
+    "cmf_ipc_open": (ctypes.c_int, [_vp, _i64, _vp]),
+    "cmf_ipc_close": (ctypes.c_int, [_vp, _i64]),
     "cmf_fused_cg_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
                                            _i32, _f64, _vp, _vp]),
+    "cmf_fused_cg_update_peers": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
+                                                 _vp, _i32, _i32, _f64, _vp, _vp]),
     "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
     "cmf_spmm_bias": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),
     "cmf_batch_cg": (ctypes.c_int, [_vp, _i32, _i64, _vp, _vp, _vp, _f64, _vp, _i64, _i32, _i32,
@@ -106,7 +111,7 @@ def check(rc: int, what: str = ""):
 
 # Kernel-launching entry points called since the counter was last reset (the
 # benchmark's "gpu_launches" claim counts launches of OUR kernels).
-_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
+_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
                 "cmf_batch_cholesky": 1, "cmf_pack_half": 1, "cmf_sq_error": 2,
                 "cmf_sq_error_csr": 2, "cmf_weighted_sqnorm": 2, "cmf_predict_pairs": 1}
 LAUNCHES = [0]

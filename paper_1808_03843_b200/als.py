@@ -172,11 +172,13 @@ class HalfUpdatePlan:
 
     def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
                row0: int = 0, nrows: int | None = None, reuse_shadow: bool = False,
-               nnz: int | None = None):
+               nnz: int | None = None, peers=None):
         """Gram(+bias) -> solve for rows [row0, row0+nrows) of the view, block by
         block, solutions written into tg (rows indexed like the view).  ``nnz``:
         ratings in those rows (default: all of the view's), which picks the
-        fused kernel's CTA shape."""
+        fused kernel's CTA shape.  ``peers``: device int64 tensor of replica
+        pointers (offset like ``tg``) that the fused kernel also stores each
+        solved row into (multi-GPU, distributed.ShardedALS)."""
         f, solver = self.f, self.solver
         nrows = self.nrows if nrows is None else nrows
         st = nat.stream_ptr()
@@ -199,10 +201,16 @@ class HalfUpdatePlan:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
             nnz = int(values.numel()) if nnz is None else int(nnz)
-            nat.call("cmf_fused_cg_update", nat.ptr(indptr) + 8 * row0, nat.ptr(indices),
-                     nat.ptr(values), nrows, nnz, nat.ptr(shadow), fx.shape[0], self.w16, f, float(lam),
-                     int(bool(weighted_reg)), nat.ptr(tg) + 4 * row0 * f, int(solver.cg_iters),
-                     float(solver.cg_tol), nat.ptr(self.flags) + 4, st)
+            common = (nat.ptr(indptr) + 8 * row0, nat.ptr(indices), nat.ptr(values), nrows, nnz,
+                      nat.ptr(shadow), fx.shape[0], self.w16, f, float(lam), int(bool(weighted_reg)),
+                      nat.ptr(tg) + 4 * row0 * f)
+            tail = (int(solver.cg_iters), float(solver.cg_tol), nat.ptr(self.flags) + 4, st)
+            if peers is not None and peers.numel():
+                if row0:
+                    raise DataError("peer stores take whole views (row0 == 0)")
+                nat.call("cmf_fused_cg_update_peers", *common, nat.ptr(peers), int(peers.numel()), *tail)
+            else:
+                nat.call("cmf_fused_cg_update", *common, *tail)
             if record is not None:
                 e1.record()
                 record.setdefault("fused_tc_cg", []).append((e0, e1))

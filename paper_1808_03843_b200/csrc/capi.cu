@@ -2,6 +2,7 @@
 // thread-local error text, and dispatch to the sm_100a kernels.
 #include <stdarg.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -26,7 +27,7 @@ int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, con
 int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, int, float, int32_t *, cudaStream_t);
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
-                    int, float *, int64_t, int, double, int32_t *, cudaStream_t);
+                    int, float *, float *const *, int, int64_t, int, double, int32_t *, cudaStream_t);
 int factors_to_half_launch(const float *, int64_t, int, void *, int, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
                      float *, cudaStream_t);
@@ -106,6 +107,50 @@ int cmf_gram_assemble(const int64_t *indptr, const int32_t *indices, const float
 
 int cmf_tc_width(int32_t f) { return gram_tc_width(f); }
 
+int cmf_ipc_export(const void *ptr, void *handle64, int64_t *offset) {
+    REQUIRE(ptr && handle64 && offset, "null argument");
+    // cudaIpcGetMemHandle wants the allocation's base; the range comes from the
+    // driver (fetched through the runtime, no libcuda link dependency)
+    typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+    static GetRange range = nullptr;
+    if (!range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return set_error(CMF_ECUDA, "cuMemGetAddressRange unavailable");
+        range = reinterpret_cast<GetRange>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+        return set_error(CMF_EINVAL, "not a device allocation");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
+    if (e != cudaSuccess) return set_error(CMF_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    memcpy(handle64, &h, sizeof(h));
+    *offset = static_cast<int64_t>(reinterpret_cast<unsigned long long>(ptr) - base);
+    return CMF_OK;
+}
+
+int cmf_ipc_open(const void *handle64, int64_t offset, void **ptr_out) {
+    REQUIRE(handle64 && ptr_out && offset >= 0, "bad argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    void *base = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return set_error(CMF_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    *ptr_out = static_cast<char *>(base) + offset;
+    return CMF_OK;
+}
+
+int cmf_ipc_close(void *ptr, int64_t offset) {
+    REQUIRE(ptr && offset >= 0, "bad argument");
+    const cudaError_t e = cudaIpcCloseMemHandle(static_cast<char *>(ptr) - offset);
+    if (e != cudaSuccess) return set_error(CMF_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return CMF_OK;
+}
+
 int cmf_debug_trace(void *buf) {
     int rc = gram_tc_trace(buf);
     return rc ? rc : fused_cg_trace(buf);
@@ -155,8 +200,25 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
     if (nrows == 0) return CMF_OK;
     REQUIRE(indptr && fixed16 && target, "null argument");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
-    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, nnz,
-                           f_s, cg_tol, breakdowns, S(stream));
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, nullptr,
+                           0, nnz, f_s, cg_tol, breakdowns, S(stream));
+}
+
+int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, const float *values,
+                              int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
+                              int32_t f, double lam, int32_t weighted_reg, float *target,
+                              float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
+                              int32_t *breakdowns, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(f_s >= 1, "cg_iters must be >= 1");
+    REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
+    REQUIRE(npeers >= 0 && npeers <= 64, "npeers must be in [0, 64]");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && fixed16 && target, "null argument");
+    REQUIRE(npeers == 0 || peer_targets, "null peer list");
+    REQUIRE(ncols >= 1, "ncols must be >= 1");
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
+                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, S(stream));
 }
 
 int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,

@@ -79,6 +79,8 @@ struct FusedArgs {
     double lam;
     int weighted;
     float *target;  // (nrows, f) in/out
+    float *const *peers;  // device array of npeers replicas of target (rows at the same index), or null
+    int npeers;
     int f_s;
     int nprod;  // active producer warps (<= F_PROD; the others exit at once)
     float tol;
@@ -480,7 +482,13 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
             cg.solve(a_tmem, dcol, reg, bi, -1.0, g.tol, g.f_s, xi, bd, nit);
             tc_fence_before();
             mbar_arrive(pp.tempty(b));  // the accumulator is free for row r_here + NBUF
-            if (act) tgt[i] = xi;
+            if (act) {
+                tgt[i] = xi;
+                // multi-GPU: the solved row also goes straight into every peer's
+                // replica (NVLink stores, coalesced 4f bytes per row), which
+                // replaces the all-gather after the half-update
+                for (int k = 0; k < g.npeers; ++k) g.peers[k][u * f + i] = xi;
+            }
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 3);
             brk += bd;
         }
@@ -662,8 +670,10 @@ static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
 
 int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
                     const void *fixed16, int64_t ncols, int W, int f, double lam, int weighted, float *target,
-                    int64_t nnz, int f_s, double cg_tol, int32_t *breakdowns, cudaStream_t st) {
+                    float *const *peers, int npeers, int64_t nnz, int f_s, double cg_tol, int32_t *breakdowns,
+                    cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
+    if (npeers < 0 || (npeers > 0 && peers == nullptr)) return set_error(CMF_EINVAL, "bad peer replica list");
     if (nnz < 0) return set_error(CMF_EINVAL, "negative rating count");
     const bool long_rows = nnz >= tc::LONG_ROW_NNZ * nrows;
     if (W + 2 > tc::M) return set_error(CMF_EINVAL, "fused CG supports f <= %d (got %d)", tc::M - 8, f);
@@ -684,6 +694,8 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
     g.lam = lam;
     g.weighted = weighted;
     g.target = target;
+    g.peers = peers;
+    g.npeers = npeers;
     g.f_s = f_s;
     {
         const char *e = getenv("CMF_FUSED_PROD");

@@ -11,6 +11,13 @@ which is the reference's epoch barrier (als.py:132-140) with the exchange
 inserted where the other half first reads the updated matrix.  With one rank
 there is no collective at all.
 
+Peer-store mode (``attach_replicas``): the ranks map each other's X / Theta
+replicas through CUDA IPC (NVLink peer memory), and the fused CG kernel
+stores every solved row into all replicas as it finishes it
+(cmf_fused_cg_update_peers), so the exchange overlaps the solve and the
+all-gather disappears; a stream sync + rank barrier orders the halves.
+Non-fused routes (exact, two-step) keep the all-gather.
+
 Shard boundaries: r_s = searchsorted(indptr, s * nnz / k, "left") -- a pure
 function of the pointer array, so every rank computes the same plan without
 communication, and concatenating the shards reproduces the reference arrays
@@ -19,9 +26,12 @@ exactly (tests/test_distributed.py).
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
+from . import _native as nat
 from .als import HalfUpdatePlan, resolve_gram_kernel
 from .errors import DataError, NumericalError
 
@@ -104,6 +114,50 @@ class ShardedALS:
         if world > 1:
             self.x_gather = RowGather(self.xb, f, dev)
             self.t_gather = RowGather(self.tb, f, dev)
+        self._replicas = None  # (x ptr, theta ptr, peers_x, peers_t, opened storages)
+
+    def attach_replicas(self, x: torch.Tensor, theta: torch.Tensor) -> bool:
+        """Map every other rank's copies of x and theta (CUDA IPC) for peer
+        stores; collective over the group.  Returns False (all-gather stays)
+        when there is a single rank or the route is not the fused kernel."""
+        import torch.distributed as dist
+        fused = self.gram_kernel == "tc" and self.solver.method == "cg"
+        if self.world == 1 or not fused:
+            return False
+        for t in (x, theta):
+            if not (t.is_cuda and t.is_contiguous() and t.dtype == torch.float32):
+                raise DataError("replicas must be contiguous float32 CUDA tensors")
+
+        def export(t):
+            h = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64()
+            nat.call("cmf_ipc_export", t.data_ptr(), ctypes.addressof(h), ctypes.addressof(off))
+            return h.raw, off.value
+
+        def open_peer(h, off):
+            buf = ctypes.create_string_buffer(h, 64)
+            ptr = ctypes.c_void_p()
+            nat.call("cmf_ipc_open", ctypes.addressof(buf), off, ctypes.addressof(ptr))
+            opened.append((ptr.value, off))
+            return ptr.value
+
+        mine = (export(x), export(theta))
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=self.group)
+        opened, px, pt = [], [], []
+        xlo, tlo = self.xb[self.rank], self.tb[self.rank]
+        for r, (hx, ht) in enumerate(everyone):
+            if r == self.rank:
+                continue
+            # my rows land at the same row index of the peer's replica
+            px.append(open_peer(*hx) + 4 * xlo * self.f)
+            pt.append(open_peer(*ht) + 4 * tlo * self.f)
+        dev = x.device
+        self._replicas = (x.data_ptr(), theta.data_ptr(),
+                          torch.tensor(px, dtype=torch.int64, device=dev),
+                          torch.tensor(pt, dtype=torch.int64, device=dev), opened)
+        dist.barrier(group=self.group)
+        return True
 
     def local_nnz(self):
         return {"x": int(self.x_view[0][-1]), "t": int(self.t_view[0][-1])}
@@ -112,13 +166,39 @@ class ShardedALS:
         return {"x": self.xb[self.rank + 1] - self.xb[self.rank],
                 "t": self.tb[self.rank + 1] - self.tb[self.rank]}
 
-    def _half(self, plan, view, fixed, target, lo, record):
+    def detach_replicas(self):
+        """Unmap the peers' replicas (after the last iteration that uses them)."""
+        if self._replicas is not None:
+            torch.cuda.synchronize()
+            for ptr, off in self._replicas[4]:
+                nat.call("cmf_ipc_close", ptr, off)
+            self._replicas = None
+
+    def _half(self, plan, view, fixed, target, lo, record, peers=None):
         ptr, idx, val = view
         # the plan writes rows [0, nrows) of the view; point it at target[lo:]
         plan.launch(ptr, idx, val, fixed, target[lo:], self.lam, self.weighted_reg,
-                    self.gram_kernel, record)
+                    self.gram_kernel, record, peers=peers)
+
+    def _peer_barrier(self, record):
+        import torch.distributed as dist
+        if record is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        torch.cuda.current_stream().synchronize()  # my peer stores are complete
+        dist.barrier(group=self.group)              # ... and everyone else's
+        if record is not None:
+            e1.record()
+            record.setdefault("peer_barrier", []).append((e0, e1))
 
     def iteration(self, x: torch.Tensor, theta: torch.Tensor, record: dict | None = None):
+        rep = self._replicas
+        if rep is not None and (rep[0], rep[1]) == (x.data_ptr(), theta.data_ptr()):
+            self._half(self.x_plan, self.x_view, theta, x, self.xb[self.rank], record, peers=rep[2])
+            self._peer_barrier(record)
+            self._half(self.t_plan, self.t_view, x, theta, self.tb[self.rank], record, peers=rep[3])
+            self._peer_barrier(record)
+            return
         self._half(self.x_plan, self.x_view, theta, x, self.xb[self.rank], record)
         if self.world > 1:
             self._gather(self.x_gather, x, record)
