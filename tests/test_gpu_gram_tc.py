@@ -125,6 +125,28 @@ def test_fused_tc_cg_matches_two_step(cuda_device):
         assert rel < 1e-4, (f, rel)
 
 
+def test_fused_tc_cg_shapes_match_two_step(cuda_device):
+    """The fused kernel's other CTA shapes against the two-step path: two CG
+    groups for f > 104, and the gather-heavy shape for views whose rows average
+    >= 1024 ratings (the item side of a tall matrix)."""
+    for f, (m, n, nnz), side in ((120, (400, 300, 24000), "csr"), (112, (300, 500, 20000), "csr"),
+                                 (100, (6000, 40, 120000), "csc"), (24, (5000, 30, 90000), "csc")):
+        t, _ = cmfb.gen_synthetic(m, n, f, nnz / (m * n), 0.1, 5)
+        sr = cmfb.build(t, m, n)
+        view = sr.csr_view() if side == "csr" else sr.csc_view()
+        if side == "csc":
+            assert sr.nnz >= 1024 * n  # exercises the long-row shape
+        rows, cols = (m, n) if side == "csr" else (n, m)
+        fixed = cmfb.init_factors(cols, f, 0.1, [0, 1])
+        outs = []
+        for kern in ("tc", "tc_unfused"):
+            x = cmfb.init_factors(rows, f, 0.1, [0, 0])
+            cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp32"), gram_kernel=kern)
+            outs.append(x)
+        rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1])
+        assert rel < 1e-4, (f, side, rel)
+
+
 def test_split_precision_gram_is_fp32_faithful(golden, oracle, cuda_device):
     """tc_split (hi/lo fp16 operands, H H^T + H L^T + L H^T) vs the reference's
     float32 Gram: within 2e-6 relative Frobenius per row -- the fp32 SIMT
