@@ -147,6 +147,24 @@ def test_fused_tc_cg_shapes_match_two_step(cuda_device):
         assert rel < 1e-4, (f, side, rel)
 
 
+def test_fused_tc_cg_large_fixed_side(cuda_device):
+    """Short rows over a fixed side too large for L2 residency (> 32 MB of
+    binary16 shadow): the fused kernel runs all 7 gather warps there."""
+    import torch
+    f = 100
+    train, _ = cmfb.gen_synthetic_device(2000, 170_000, f, 100_000, 0.1, 0.1, seed=2)
+    view = train.csr_view()
+    assert 170_000 * 104 * 2 > (32 << 20)
+    fixed = torch.from_numpy(cmfb.init_factors(170_000, f, 0.1, [0, 1])).cuda()
+    outs = []
+    for kern in ("tc", "tc_unfused"):
+        x = torch.from_numpy(cmfb.init_factors(2000, f, 0.1, [0, 0])).cuda()
+        cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp32"), gram_kernel=kern)
+        outs.append(x)
+    rel = float(torch.linalg.norm(outs[0] - outs[1]) / torch.linalg.norm(outs[1]))
+    assert rel < 1e-4, rel
+
+
 def test_split_precision_gram_is_fp32_faithful(golden, oracle, cuda_device):
     """tc_split (hi/lo fp16 operands, H H^T + H L^T + L H^T) vs the reference's
     float32 Gram: within 2e-6 relative Frobenius per row -- the fp32 SIMT
