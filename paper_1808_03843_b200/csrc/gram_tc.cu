@@ -232,13 +232,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
 
 // fp32 (rows, f) -> binary16 (rows + 1, W), zero padded, RNE; row `rows` is the
 // all-zero row the gather reads for padding positions.
+// One warp per shadow row (rows + 1 of them, the last all zero), 4 halves per
+// lane: 16-byte coalesced loads, 8-byte stores, no per-element index division.
 __global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __half *out, int W) {
-    const int64_t n = (rows + 1) * W;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
-        const int64_t r = e / W;
-        const int c = static_cast<int>(e - r * W);
-        out[e] = (c < f && r < rows) ? __float2half_rn(x[r * f + c]) : __float2half_rn(0.0f);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r <= rows; r += nw) {
+        const float *src = x + r * f;
+        for (int c = 4 * lane; c < W; c += 128) {
+            float v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = (r < rows && c + k < f) ? src[c + k] : 0.0f;
+            const __half2 h01 = __floats2half2_rn(v[0], v[1]), h23 = __floats2half2_rn(v[2], v[3]);
+            *reinterpret_cast<uint2 *>(out + r * W + c) =
+                make_uint2(*reinterpret_cast<const uint32_t *>(&h01), *reinterpret_cast<const uint32_t *>(&h23));
+        }
     }
 }
 
@@ -246,17 +254,24 @@ __global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __ha
 // two that keeps lo out of the binary16 subnormal range for |x| >= 2^-9.
 __global__ void factors_to_half_split_kernel(const float *x, int64_t rows, int f, __half *hi, __half *lo, int W,
                                              float scale, int32_t *ovf) {
-    const int64_t n = (rows + 1) * W;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     int bad = 0;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
-        const int64_t r = e / W;
-        const int c = static_cast<int>(e - r * W);
-        const float v = (c < f && r < rows) ? x[r * f + c] * scale : 0.0f;
-        const __half h = __float2half_rn(v);
-        if (isfinite(v) && __hisinf(h)) bad = 1;
-        hi[e] = h;
-        lo[e] = __float2half_rn(v - __half2float(h));
+    for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r <= rows; r += nw) {
+        const float *src = x + r * f;
+        for (int c = 4 * lane; c < W; c += 128) {
+            __align__(8) __half h[4];
+            __align__(8) __half l[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float v = (r < rows && c + k < f) ? src[c + k] * scale : 0.0f;
+                h[k] = __float2half_rn(v);
+                if (isfinite(v) && __hisinf(h[k])) bad = 1;
+                l[k] = __float2half_rn(v - __half2float(h[k]));
+            }
+            *reinterpret_cast<uint2 *>(hi + r * W + c) = *reinterpret_cast<const uint2 *>(h);
+            *reinterpret_cast<uint2 *>(lo + r * W + c) = *reinterpret_cast<const uint2 *>(l);
+        }
     }
     if (bad && ovf) atomicOr(ovf, 1);
 }
@@ -266,7 +281,7 @@ __global__ void factors_to_half_split_kernel(const float *x, int64_t rows, int f
 int factors_to_half_split_launch(const float *x, int64_t rows, int f, void *hi, void *lo, int W, float scale,
                                  int32_t *ovf, cudaStream_t st) {
     if (rows == 0) return CMF_OK;
-    int64_t blocks = ((rows + 1) * W + 255) / 256;
+    int64_t blocks = (rows + 1 + 7) / 8;  // 8 rows (warps) per 256-thread block
     if (blocks > 148 * 16) blocks = 148 * 16;
     tc::factors_to_half_split_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         x, rows, f, static_cast<__half *>(hi), static_cast<__half *>(lo), W, scale, ovf);
@@ -279,7 +294,7 @@ int gram_tc_width(int f) { return ((f + 7) / 8) * 8; }
 
 int factors_to_half_launch(const float *x, int64_t rows, int f, void *out, int W, cudaStream_t st) {
     if (rows == 0) return CMF_OK;
-    int64_t blocks = ((rows + 1) * W + 255) / 256;
+    int64_t blocks = (rows + 1 + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
     tc::factors_to_half_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, rows, f,
                                                                              static_cast<__half *>(out), W);
