@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttr", action="store_true", help="skip time-to-RMSE")
+    ap.add_argument("--no-next", action="store_true",
+                    help="skip the SURVEY 8(f) rows (implicit iteration, eval, build)")
     ap.add_argument("--cpu-sample-nnz", type=int, default=4_000_000)
     return ap.parse_args()
 
@@ -448,6 +450,12 @@ def main():
         del ex_engine
 
     # ---- time to RMSE (fresh start; per-epoch eval excluded from the clock)
+    # ---- SURVEY 8(f) rows on the same data: implicit ALS iteration (f1, |r| as
+    #      the interaction strength, alpha = 40), test RMSE / objective (f2),
+    #      CSR + CSC build from device triples (f3); device time, N = 1
+    if not args.no_next and world == 1:
+        result["next_rows"] = next_rows(cmfb, train, test, x0, th0, m, n)
+
     if not args.no_ttr and world == 1:
         result["time_to_rmse"] = time_to_rmse(cmfb, engine, train, test, x0, th0, f)
 
@@ -470,6 +478,43 @@ def main():
     emit(result, rank)
     if world > 1:
         dist.destroy_process_group()
+
+
+def next_rows(cmfb, train, test, x0, th0, m, n):
+    import torch
+    from paper_1808_03843_b200.implicit import implicit_update_side, precompute_gram
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    out = {}
+    users = torch.repeat_interleave(torch.arange(m, device="cuda"), train.row_ptr.diff())
+    trip = cmfb.Triples(users, train.col_idx.to(torch.int64), train.csr_val)
+    out["build_csr_csc_ms"] = timed(lambda: cmfb.build_device(trip, m, n), 1)
+    del users, trip
+    x, th = x0.clone(), th0.clone()
+    out["test_rmse_ms"] = timed(lambda: cmfb.rmse(x, th, test), 3)
+    out["objective_ms"] = timed(lambda: cmfb.objective(x, th, train, 0.05), 3)
+    solver = cmfb.SolverConfig("cg")
+    csr = cmfb.RowView(train.row_ptr, train.col_idx, train.csr_val.abs(), m, n)
+    csc = cmfb.RowView(train.col_ptr, train.row_idx, train.csc_val.abs(), n, m)
+
+    def implicit_iteration():
+        implicit_update_side(csr, th, precompute_gram(th), x, 40.0, 0.05, solver, gram_kernel="fma")
+        implicit_update_side(csc, x, precompute_gram(x), th, 40.0, 0.05, solver, gram_kernel="fma")
+
+    out["implicit_iteration_ms"] = timed(implicit_iteration, 2)
+    out["note"] = ("device time on the bench data; implicit = weighted FMA Gram + CG fp32, "
+                   "f_s = 6 (the tensor-core route has no per-rating operand weights yet)")
+    return out
 
 
 def time_to_rmse(cmfb, engine, train, test, x0, th0, f, max_epochs=10):
