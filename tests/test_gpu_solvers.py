@@ -118,3 +118,27 @@ def test_batch_validation(cuda_device):
     h = cmfb.GramSystem(3, cmfb.pack_half(cmfb.pack_lower(np.eye(3))), np.ones(3, np.float32), 1)
     with pytest.raises(cmfb.DataError):
         cmfb.batch_solve([h], np.zeros((1, 3), np.float32), cmfb.SolverConfig("exact"))
+
+
+@pytest.mark.parametrize("f", [1, 3, 4, 5, 7, 8, 31, 64, 97, 100, 113, 127, 128])
+def test_batched_cholesky_sizes(cuda_device, f):
+    """The shared-memory tile Cholesky (f <= 128) at every padding case (f % 4),
+    single-tile and full-width systems, with a non-SPD system in the batch: it is
+    reported (rows) while every other system is solved to fp32 accuracy."""
+    rng = np.random.default_rng(f)
+    nsys = 40
+    a_list, b = [], rng.standard_normal((nsys, f)).astype(np.float32)
+    for s in range(nsys):
+        q, _ = np.linalg.qr(rng.standard_normal((f, f)))
+        a_list.append((q * np.geomspace(1.0, 30.0, f)) @ q.T)
+    packed = np.stack([cmfb.pack_lower(a) for a in a_list]).astype(np.float32)
+    r = cmfb.batch_solve(_batch(packed, b), np.zeros((nsys, f), np.float32), cmfb.SolverConfig("exact"))
+    for s in range(nsys):
+        full = cmfb.unpack_lower(packed[s].astype(np.float64), f)
+        ref = np.linalg.solve(full, b[s].astype(np.float64))
+        assert np.linalg.norm(r.x[s] - ref) / np.linalg.norm(ref) <= 1e-5 * 30, (f, s)
+    bad = packed.copy()
+    bad[7] = cmfb.pack_lower(-np.eye(f)).astype(np.float32)
+    with pytest.raises(cmfb.SingularSystemError) as e:
+        cmfb.batch_solve(_batch(bad, b), np.zeros((nsys, f), np.float32), cmfb.SolverConfig("exact"))
+    assert e.value.rows == [7]
