@@ -587,22 +587,26 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
         named_bar(1 + grp, CG_THREADS);
         // row i of the symmetric matrix -> binary16 pairs in TMEM
         const __half *A = reinterpret_cast<const __half *>(stg + buf * SB);
-        const int64_t ri = static_cast<int64_t>(i) * (i + 1) / 2;
+        // element (i, j): row i of the packed lower triangle for j <= i, column i
+        // (row j, position i) above the diagonal; j is warp-uniform, so the
+        // column reads of a warp are consecutive halves.  32-bit offsets; lanes
+        // i >= f read element 0 (their rows only feed their own, unused outputs)
+        const int ri = act ? i * (i + 1) / 2 : 0;
+        const int ci = act ? i : 0;
+        const unsigned short *Au = reinterpret_cast<const unsigned short *>(A);
 #pragma unroll 1
         for (int c = 0; c < (KP + 31) / 32; ++c) {
             uint32_t h[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                uint16_t e[2];
+                uint32_t e[2];
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     const int j = 32 * c + 2 * q + t;
-                    uint16_t v = 0;
-                    if (act && j < f)
-                        v = __half_as_ushort(j <= i ? A[ri + j] : A[static_cast<int64_t>(j) * (j + 1) / 2 + i]);
-                    e[t] = v;
+                    e[t] = 0u;
+                    if (j < f) e[t] = Au[j <= ci ? ri + j : j * (j + 1) / 2 + ci];
                 }
-                h[q] = static_cast<uint32_t>(e[0]) | (static_cast<uint32_t>(e[1]) << 16);
+                h[q] = e[0] | (e[1] << 16);
             }
             if (16 * c + 16 <= KP / 2) tmem_st16(slot_t + 16 * c, h);
             else if (16 * c < KP / 2) tmem_st8(slot_t + 16 * c, h);
