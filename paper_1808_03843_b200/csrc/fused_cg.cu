@@ -594,8 +594,8 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
         const int ri = act ? i * (i + 1) / 2 : 0;
         const int ci = act ? i : 0;
         const unsigned short *Au = reinterpret_cast<const unsigned short *>(A);
-#pragma unroll 1
-        for (int c = 0; c < (KP + 31) / 32; ++c) {
+#pragma unroll
+        for (int c = 0; c < (KP + 31) / 32; ++c) {  // fully unrolled: j, j(j+1)/2 are immediates
             uint32_t h[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
