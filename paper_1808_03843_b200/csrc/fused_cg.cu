@@ -313,7 +313,8 @@ struct TmemCg {
                                    float &xi, int &bd, int &nit) {
         float bb, rs, unused;
         float r = bi - exchange(a_tmem, dcol, 0.0f, xi, bi * bi, 0.0f, bb, unused, true);
-        const double e = eps >= 0.0 ? eps : static_cast<double>(tol) * sqrt(static_cast<double>(bb));
+        // stop test ||r|| < eps as r.r < eps^2 in fp32 (no double sqrt per iteration)
+        const float e2 = eps >= 0.0 ? static_cast<float>(eps * eps) : tol * tol * bb;
         exchange(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs, unused, false);
         float p = r;
         bd = 0;
@@ -326,13 +327,13 @@ struct TmemCg {
                 bd = 1;
                 break;
             }
-            const float alpha = rs / pap;
+            const float alpha = __fdividef(rs, pap);
             xi = fmaf(alpha, p, xi);
             r = fmaf(-alpha, ap, r);
             exchange(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs_new, unused, false);
             ++nit;
-            if (rs_new == 0.0f || sqrt(static_cast<double>(rs_new)) < e) break;
-            p = fmaf(rs_new / rs, p, r);
+            if (rs_new == 0.0f || rs_new < e2) break;
+            p = fmaf(__fdividef(rs_new, rs), p, r);
             rs = rs_new;
         }
     }
