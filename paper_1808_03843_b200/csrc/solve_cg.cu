@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(128) cg_rowreg_kernel(CgArgs g) {
         eps = g.tol * sqrt(bn);
     }
 
+    const float eps2 = static_cast<float>(eps * eps);
     int slot = 0;
     auto bsum = [&](float v) {
         float r = block_sum<float>(v, red + 32 * slot);
@@ -143,13 +144,13 @@ __global__ void __launch_bounds__(128) cg_rowreg_kernel(CgArgs g) {
             bd = 1;
             break;
         }
-        const float alpha = rs_old / pap;
+        const float alpha = __fdividef(rs_old, pap);
         xi = fmaf(alpha, p, xi);
         r = fmaf(-alpha, ap, r);
         const float rs_new = bsum(r * r);
         ++it;
-        if (rs_new == 0.0f || sqrt(static_cast<double>(rs_new)) < eps) break;
-        const float beta = rs_new / rs_old;
+        if (rs_new == 0.0f || rs_new < eps2) break;  // ||r|| < eps, squared in fp32
+        const float beta = __fdividef(rs_new, rs_old);
         p = fmaf(beta, p, r);
         rs_old = rs_new;
     }
