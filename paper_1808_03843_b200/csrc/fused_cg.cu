@@ -245,6 +245,8 @@ struct TmemCg {
 
     // y_i = (A v)_i + reg * v_i and (sa, sb) = group sums of (da, db); rows i >= f
     // (act == false) publish nothing and return 0
+    // NRED: how many of (da, db) are reduced (0, 1 or 2); the others return 0
+    template <int NRED = 2>
     __device__ float exchange(uint32_t a_tmem, uint32_t dcol, float reg, float v, float da, float db, float &sa,
                               float &sb, bool mv) {
         constexpr uint32_t idesc_mv = (1u << 4) | (static_cast<uint32_t>(16 >> 3) << 17) |
@@ -261,14 +263,14 @@ struct TmemCg {
         // per value are summed after the barrier in a fixed order
 #pragma unroll
         for (int o = 16; o > 2; o >>= 1) {
-            da += __shfl_xor_sync(0xffffffffu, da, o);
-            db += __shfl_xor_sync(0xffffffffu, db, o);
+            if (NRED >= 1) da += __shfl_xor_sync(0xffffffffu, da, o);
+            if (NRED >= 2) db += __shfl_xor_sync(0xffffffffu, db, o);
         }
         float *rd = red + 32 * slot;
         slot ^= 1;
         if (lane < 4) {
-            rd[(warp & 3) * 4 + lane] = da;
-            rd[16 + (warp & 3) * 4 + lane] = db;
+            if (NRED >= 1) rd[(warp & 3) * 4 + lane] = da;
+            if (NRED >= 2) rd[16 + (warp & 3) * 4 + lane] = db;
         }
         named_bar(bar_id, CG_THREADS);
         CG_STAMP();
@@ -287,12 +289,12 @@ struct TmemCg {
             const float4 *r4 = reinterpret_cast<const float4 *>(rd);
             float t[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < 4 * NRED; ++k) {
                 const float4 q = r4[k];
                 t[k] = (q.x + q.y) + (q.z + q.w);
             }
-            sa = (t[0] + t[1]) + (t[2] + t[3]);
-            sb = (t[4] + t[5]) + (t[6] + t[7]);
+            sa = NRED >= 1 ? (t[0] + t[1]) + (t[2] + t[3]) : 0.0f;
+            sb = NRED >= 2 ? (t[4] + t[5]) + (t[6] + t[7]) : 0.0f;
         }
         if (!mv) return 0.0f;
         mbar_wait(mvbar, mvph & 1);
@@ -312,17 +314,17 @@ struct TmemCg {
     __device__ void solve_standard(uint32_t a_tmem, uint32_t dcol, float bi, double eps, float tol, int f_s,
                                    float &xi, int &bd, int &nit) {
         float bb, rs, unused;
-        float r = bi - exchange(a_tmem, dcol, 0.0f, xi, bi * bi, 0.0f, bb, unused, true);
+        float r = bi - exchange<1>(a_tmem, dcol, 0.0f, xi, bi * bi, 0.0f, bb, unused, true);
         // stop test ||r|| < eps as r.r < eps^2 in fp32 (no double sqrt per iteration)
         const float e2 = eps >= 0.0 ? static_cast<float>(eps * eps) : tol * tol * bb;
-        exchange(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs, unused, false);
+        exchange<1>(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs, unused, false);
         float p = r;
         bd = 0;
         nit = 0;
         for (int step = 0; step < f_s; ++step) {
             float pap, rs_new;
-            const float ap = exchange(a_tmem, dcol, 0.0f, p, 0.0f, 0.0f, unused, unused, true);
-            exchange(a_tmem, dcol, 0.0f, 0.0f, p * ap, 0.0f, pap, unused, false);
+            const float ap = exchange<0>(a_tmem, dcol, 0.0f, p, 0.0f, 0.0f, unused, unused, true);
+            exchange<1>(a_tmem, dcol, 0.0f, 0.0f, p * ap, 0.0f, pap, unused, false);
             if (!(pap > 0.0f)) {
                 bd = 1;
                 break;
@@ -330,7 +332,7 @@ struct TmemCg {
             const float alpha = __fdividef(rs, pap);
             xi = fmaf(alpha, p, xi);
             r = fmaf(-alpha, ap, r);
-            exchange(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs_new, unused, false);
+            exchange<1>(a_tmem, dcol, 0.0f, 0.0f, r * r, 0.0f, rs_new, unused, false);
             ++nit;
             if (rs_new == 0.0f || rs_new < e2) break;
             p = fmaf(__fdividef(rs_new, rs), p, r);
@@ -342,10 +344,10 @@ struct TmemCg {
     __device__ void solve(uint32_t a_tmem, uint32_t dcol, float reg, float bi, double eps, float tol, int f_s,
                           float &xi, int &bd, int &nit) {
         float bb, unused;
-        float r = bi - exchange(a_tmem, dcol, reg, xi, bi * bi, 0.0f, bb, unused, true);
+        float r = bi - exchange<1>(a_tmem, dcol, reg, xi, bi * bi, 0.0f, bb, unused, true);
         const float eps2 = eps >= 0.0 ? static_cast<float>(eps * eps) : tol * tol * bb;
         float gamma, delta;
-        float w = exchange(a_tmem, dcol, reg, r, 0.0f, 0.0f, gamma, delta, true);
+        float w = exchange<0>(a_tmem, dcol, reg, r, 0.0f, 0.0f, gamma, delta, true);
         // 1/gamma_old and 1/alpha_old are formed off the critical path (one
         // iteration early); only 1/pap sits on it.  rcp.approx (1 ulp): the
         // scalars feed a truncated CG graded on the RMSE trajectory.
