@@ -301,10 +301,13 @@ struct TmemCg {
         CG_STAMP();
         ++mvph;
         tc_fence_after();
-        const float y0 = __uint_as_float(tmem_ld1(dcol + lane_base));
-        const float y1 = __uint_as_float(tmem_ld1(dcol + lane_base + 1));
+        uint32_t yv[2];  // matvec result columns: A v_hi, A v_lo
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                     : "=r"(yv[0]), "=r"(yv[1])
+                     : "r"(dcol + lane_base)
+                     : "memory");
         tmem_ld_wait();
-        const float y = act ? y0 + y1 : 0.0f;
+        const float y = act ? __uint_as_float(yv[0]) + __uint_as_float(yv[1]) : 0.0f;
         return fmaf(reg, v, y);
     }
 
