@@ -48,6 +48,13 @@ def _compile(src, force, hdr_mtime):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    # objects built with other flags (e.g. CMF_NVCC_EXTRA=-DCMF_TRACE) are stale
+    stamp = os.path.join(OBJ, "flags.txt")
+    flags = " ".join([NVCC, *ARCH, *FLAGS])
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
+        with open(stamp, "w") as fh:
+            fh.write(flags)
     srcs = _sources()
     hm = _headers_mtime()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
