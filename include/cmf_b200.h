@@ -119,14 +119,18 @@ int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi1
  * solved in place, target[u] <- CG_{f_s}(A_u + reg*I, b_u, x0 = target[u]),
  * eps = cg_tol * ||b_u||.  A_u never reaches HBM.  Replaces als.update_side
  * (als.py:54-74) for SolverConfig(method="cg").  f <= 120.  *breakdowns
- * (device int, nullable) accumulates p^T A p <= 0 exits.  nnz =
+ * (device int, nullable) accumulates p^T A p <= 0 exits.  A_u is used by the
+ * CG in binary16 (RNE, the reference's precision="fp16" Hermitian storage,
+ * gram.py:132-146): an entry of a row's A_u (or a rating) whose binary16
+ * rounding overflows sets *overflow_flag (device int, nullable, caller zeroes
+ * it; the caller raises NumericalError).  nnz =
  * indptr[nrows] - indptr[0], counted on the host: rows averaging >= 1024
  * ratings (the item side) run a CTA shape with fewer CG warps.
  */
 int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
                         int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
                         int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
-                        int32_t *breakdowns, void *stream);
+                        int32_t *breakdowns, int32_t *overflow_flag, void *stream);
 /*
  * Multi-GPU form of cmf_fused_cg_update: every solved row is also stored into
  * npeers replicas of `target` (peer_targets: a DEVICE array of device
@@ -139,7 +143,7 @@ int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, con
                               int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
                               int32_t f, double lam, int32_t weighted_reg, float *target,
                               float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
-                              int32_t *breakdowns, void *stream);
+                              int32_t *breakdowns, int32_t *overflow_flag, void *stream);
 /* CUDA IPC for the peer replicas: export a device pointer (any address inside
  * an allocation) as a 64-byte handle + offset; open it in another process
  * (peer access enabled lazily over NVLink); close with the same offset. */
@@ -154,9 +158,11 @@ int cmf_debug_trace(void *buf);
 int cmf_tc_width(int32_t f);
 /* fp32 (rows, f) -> binary16 (rows + 1, w16), RNE, zero padded columns, plus an
  * all-zero row `rows`: the tensor-core gather reads it for padding positions
- * (and for column ids >= ncols), so out16 must hold (rows + 1) * w16 halves. */
+ * (and for column ids >= ncols), so out16 must hold (rows + 1) * w16 halves.
+ * A finite value whose binary16 rounding overflows sets *overflow_flag
+ * (nullable). */
 int cmf_factors_to_half(const float *x, int64_t rows, int32_t f, void *out16, int32_t w16,
-                        void *stream);
+                        int32_t *overflow_flag, void *stream);
 
 /*
  * K2 alone: b_u = sum_p b_w[p] * theta_{indices[p]}, float64 accumulation in

@@ -45,10 +45,10 @@ _SIGNATURES = {
     "cmf_ipc_open": (ctypes.c_int, [_vp, _i64, _vp]),
     "cmf_ipc_close": (ctypes.c_int, [_vp, _i64]),
     "cmf_fused_cg_update": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
-                                           _i32, _f64, _vp, _vp]),
+                                           _i32, _f64, _vp, _vp, _vp]),
     "cmf_fused_cg_update_peers": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
-                                                 _vp, _i32, _i32, _f64, _vp, _vp]),
-    "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
+                                                 _vp, _i32, _i32, _f64, _vp, _vp, _vp]),
+    "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp]),
     "cmf_spmm_bias": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),
     "cmf_batch_cg": (ctypes.c_int, [_vp, _i32, _i64, _vp, _vp, _vp, _f64, _vp, _i64, _i32, _i32,
                                     _i32, _vp, _vp, _vp, _vp, _vp]),

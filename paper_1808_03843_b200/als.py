@@ -29,7 +29,7 @@ from .errors import DataError, NumericalError
 from .factors import init_factors
 from .gram import TileConfig, packed_size, roofline_estimate
 from .report import EpochRecord, PhaseTimes, TrainReport
-from .solvers import SolverConfig, _singular_error
+from .solvers import SolverConfig, _singular_error, with_accum
 
 WORKSPACE_BYTES = int(float(os.environ.get("CMF_WORKSPACE_GB", "16")) * (1 << 30))
 
@@ -68,23 +68,36 @@ SPLIT_SCALE = 64.0  # split-fp16 shadow scale: lo stays normal for |theta| >= 2^
 def resolve_gram_kernel(kernel: str | None, solver: SolverConfig, f: int | None = None) -> str:
     """Kernel choice for update_side/train.
 
-    "auto": the CG route runs fused on the tensor cores ("tc": Gram in TMEM,
-    CG in registers, A never stored) when f <= 120; the exact route uses the
+    "auto": the CG route with binary16 Hermitian storage (precision="fp16",
+    the paper's approximate route) runs fused on the tensor cores ("tc": Gram
+    in TMEM, repacked to binary16 there, CG matvecs on the tensor core, A never
+    stored) when f <= 120.  precision="fp32" keeps fp32 storage: the
     split-precision tensor-core Gram ("tc_split": hi/lo fp16 operands, three
-    MMAs, fp32-faithful -- the 1e-4 factor bar rules out a single fp16/TF32
-    pass) and falls back to the SIMT FMA Gram for larger f.
+    MMAs, fp32-faithful) writes fp32 packed systems that the fp32 CG (or the
+    Cholesky) reads -- the same route the exact solver takes, since the 1e-4
+    factor bar rules out a single fp16/TF32 pass.  accum="fp64"
+    also leaves the fused kernel (its vectors are fp32): "tc_unfused" for
+    fp16 storage.  Larger f falls back to the SIMT FMA Gram.
     "tc_unfused" is the paper's two-step scheme on the tensor cores: packed
     fp16/fp32 A_u written to HBM, then the batched CG kernel reads it.
+    An explicit "tc" with precision="fp32" or accum="fp64" is refused
+    (DataError): the fused kernel computes in binary16/fp32 only.
     """
+    solver = with_accum(solver, "fp32")
     if kernel in (None, "auto"):
         kernel = os.environ.get("CMF_TRAIN_GRAM_KERNEL", "auto")
     small = f is None or f <= TC_MAX_F
     if kernel == "auto":
-        if solver.method == "cg":
-            return "tc" if small else "fma"
-        return "tc_split" if small else "fma"
+        if not small:
+            return "fma"
+        if solver.method == "cg" and solver.precision == "fp16":
+            return "tc" if solver.accum == "fp32" else "tc_unfused"
+        return "tc_split"
     if kernel not in nat.GRAM_KERNELS:
         raise DataError(f"unknown gram kernel {kernel!r}")
+    if kernel == "tc" and solver.method == "cg" and (solver.precision != "fp16" or solver.accum != "fp32"):
+        raise DataError("the fused tensor-core CG kernel stores A_u in binary16 and runs fp32 vectors; "
+                        "use precision='fp16', accum='fp32' (or gram_kernel='tc_unfused' / 'tc_split')")
     if kernel in ("tc", "tc_unfused") and solver.method == "exact":
         raise DataError("the single-pass fp16 tensor-core Gram cannot feed the exact solver; "
                         "use gram_kernel='tc_split', 'fma' or 'bitwise'")
@@ -131,6 +144,7 @@ class HalfUpdatePlan:
 
     def __init__(self, nrows: int, f: int, solver: SolverConfig, dev,
                  workspace_bytes: int | None = None):
+        solver = with_accum(solver, "fp32")
         self.f, self.solver, self.nrows, self.dev = f, solver, nrows, dev
         self.half = solver.precision == "fp16"
         self.esize = 2 if self.half else 4
@@ -167,7 +181,7 @@ class HalfUpdatePlan:
                      nat.ptr(self.flags), nat.stream_ptr())
             return self.shadow, nat.ptr(self.shadow) + 2 * half
         nat.call("cmf_factors_to_half", nat.ptr(fx), fx.shape[0], self.f, nat.ptr(self.shadow),
-                 self.w16, nat.stream_ptr())
+                 self.w16, nat.ptr(self.flags), nat.stream_ptr())
         return self.shadow, None
 
     def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
@@ -204,7 +218,8 @@ class HalfUpdatePlan:
             common = (nat.ptr(indptr) + 8 * row0, nat.ptr(indices), nat.ptr(values), nrows, nnz,
                       nat.ptr(shadow), fx.shape[0], self.w16, f, float(lam), int(bool(weighted_reg)),
                       nat.ptr(tg) + 4 * row0 * f)
-            tail = (int(solver.cg_iters), float(solver.cg_tol), nat.ptr(self.flags) + 4, st)
+            tail = (int(solver.cg_iters), float(solver.cg_tol), nat.ptr(self.flags) + 4,
+                    nat.ptr(self.flags), st)
             if peers is not None and peers.numel():
                 if row0:
                     raise DataError("peer stores take whole views (row0 == 0)")
@@ -293,8 +308,7 @@ def update_side(view: RowView, fixed, target, lam: float, solver: SolverConfig,
     plan.launch(indptr, indices, values, fx, tg, lam, weighted_reg, kernel, rec)
     fl = plan.read_flags()
     if fl[0]:
-        raise NumericalError("Gram entries overflow binary16 range (+-65504); "
-                             "rescale the ratings before using half precision")
+        raise NumericalError(_OVERFLOW_MSG)
     if fl[2]:
         raise _locate_singular(indptr, indices, values, nrows, fx, f, lam, weighted_reg,
                                kernel, solver)
@@ -314,6 +328,9 @@ def update_side(view: RowView, fixed, target, lam: float, solver: SolverConfig,
             target[...] = nat.to_host(tg)
     return times, nrows * packed_size(f) * plan.esize, int(fl[1])
 
+
+_OVERFLOW_MSG = ("Gram entries overflow binary16 range (+-65504); "
+                 "rescale the ratings before using half precision")
 
 STREAM_CHUNKS = int(os.environ.get("CMF_STREAM_CHUNKS", "8"))
 STREAM_MIN_ROWS = 4096
@@ -348,6 +365,9 @@ def _update_side_streamed(view: RowView, fixed, target, lam, solver, weighted_re
     fx = torch.empty(fixed.shape, dtype=torch.float32, device=dev)
     tg = torch.empty(target.shape, dtype=torch.float32, device=dev)
     plan = HalfUpdatePlan(nrows, f, solver, dev)
+    # the buffers above were allocated on the compute stream: a block the caching
+    # allocator recycled may still be read by a kernel queued there
+    h2d.wait_stream(comp)
     with torch.cuda.stream(h2d):
         fx.copy_(fixed, non_blocking=True)
         indptr.copy_(indptr_h, non_blocking=True)
@@ -380,6 +400,8 @@ def _update_side_streamed(view: RowView, fixed, target, lam, solver, weighted_re
         t.record_stream(d2h)
     d2h.synchronize()
     fl = plan.read_flags()
+    if fl[0]:
+        raise NumericalError(_OVERFLOW_MSG)
     times = PhaseTimes()
     for name, ms in resolve_events(rec).items():
         times.accumulate += sum(ms) / 1e3
@@ -390,13 +412,17 @@ def _locate_singular(indptr, indices, values, nrows, fx, f, lam, weighted_reg, k
     """Recompute the side with per-system info to name the failing rows, numbered
     among rows with n_u > 0 as the reference's compacted batch does (als.py:69-71)."""
     dev = fx.device
+    solver = with_accum(solver, "fp32")
     P = packed_size(f)
     a = torch.empty((nrows, P), dtype=torch.float32, device=dev)
     b = torch.empty((nrows, f), dtype=torch.float32, device=dev)
     nu = torch.empty(nrows, dtype=torch.int64, device=dev)
+    # the SIMT Gram names the rows for every route (the tensor-core kernels have
+    # their own entry point; which rows are singular does not depend on it)
+    simt = kernel if kernel in ("bitwise", "fma") else "fma"
     nat.call("cmf_gram_assemble", nat.ptr(indptr), nat.ptr(indices), None, nat.ptr(values), nrows,
              nat.ptr(fx), fx.shape[0], f, float(lam), int(bool(weighted_reg)), None, 0,
-             nat.GRAM_KERNELS[kernel], nat.ptr(a), P, nat.ptr(b), nat.ptr(nu), None,
+             nat.GRAM_KERNELS[simt], nat.ptr(a), P, nat.ptr(b), nat.ptr(nu), None,
              nat.stream_ptr())
     out = torch.empty_like(b)
     info = torch.zeros(nrows, dtype=torch.int32, device=dev)

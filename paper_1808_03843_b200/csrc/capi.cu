@@ -27,8 +27,8 @@ int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, con
 int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, int, float, int32_t *, cudaStream_t);
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
-                    int, float *, float *const *, int, int64_t, int, double, int32_t *, cudaStream_t);
-int factors_to_half_launch(const float *, int64_t, int, void *, int, cudaStream_t);
+                    int, float *, float *const *, int, int64_t, int, double, int32_t *, int32_t *, cudaStream_t);
+int factors_to_half_launch(const float *, int64_t, int, void *, int, int32_t *, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
                      float *, cudaStream_t);
 int cg_launch(const void *, bool, int64_t, const float *, const float *, const double *, double,
@@ -157,11 +157,11 @@ int cmf_debug_trace(void *buf) {
 }
 
 int cmf_factors_to_half(const float *x, int64_t rows, int32_t f, void *out16, int32_t w16,
-                        void *stream) {
+                        int32_t *overflow_flag, void *stream) {
     REQUIRE(rows >= 0 && f >= 1 && w16 >= f, "bad dimensions");
     if (rows == 0) return CMF_OK;
     REQUIRE(x && out16, "null argument");
-    return factors_to_half_launch(x, rows, f, out16, w16, S(stream));
+    return factors_to_half_launch(x, rows, f, out16, w16, overflow_flag, S(stream));
 }
 
 int cmf_factors_to_half_split(const float *x, int64_t rows, int32_t f, void *hi16, void *lo16, int32_t w16,
@@ -193,7 +193,7 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
 int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,
                         int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
                         int32_t weighted_reg, float *target, int32_t f_s, double cg_tol,
-                        int32_t *breakdowns, void *stream) {
+                        int32_t *breakdowns, int32_t *overflow_flag, void *stream) {
     REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
     REQUIRE(f_s >= 1, "cg_iters must be >= 1");
     REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
@@ -201,14 +201,14 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
     REQUIRE(indptr && fixed16 && target, "null argument");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, nullptr,
-                           0, nnz, f_s, cg_tol, breakdowns, S(stream));
+                           0, nnz, f_s, cg_tol, breakdowns, overflow_flag, S(stream));
 }
 
 int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, const float *values,
                               int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
                               int32_t f, double lam, int32_t weighted_reg, float *target,
                               float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
-                              int32_t *breakdowns, void *stream) {
+                              int32_t *breakdowns, int32_t *overflow_flag, void *stream) {
     REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
     REQUIRE(f_s >= 1, "cg_iters must be >= 1");
     REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
@@ -218,7 +218,7 @@ int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, con
     REQUIRE(npeers == 0 || peer_targets, "null peer list");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
-                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, S(stream));
+                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, S(stream));
 }
 
 int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,
@@ -274,7 +274,7 @@ int cmf_half_update(const int64_t *indptr, const int32_t *indices, const float *
     const int w16 = gram_tc_width(f);
     if (kernel == CMF_GRAM_TC) {
         REQUIRE(ws16, "CMF_GRAM_TC needs the ws16 shadow buffer");
-        int rc = factors_to_half_launch(fixed, ncols, f, ws16, w16, st);
+        int rc = factors_to_half_launch(fixed, ncols, f, ws16, w16, flags + 0, st);
         if (rc) return rc;
     }
     for (int64_t r0 = 0; r0 < nrows; r0 += ws_rows) {

@@ -13,23 +13,25 @@
 //                          rows) into a 12-stage swizzled operand ring
 //   warp 19     MMA        tcgen05.mma kind::f16 chain per row into TMEM buffer
 //                          (row % 3); tcgen05.commit -> stage empty / tmem full
-//   warps 0-11  CG         three groups of 4 warps, one per TMEM buffer: load the
-//                          row's A_u and b_u from TMEM (fp32), free the buffer,
-//                          run Algorithm 1 (corrected
-//                          r -= alpha*A p) in its pipelined form (one barrier
-//                          per iteration carries both dot products and the
-//                          next matvec's vector) with fp32 vectors; A_u stays
-//                          in TMEM and each matvec streams the thread's row in
-//                          32-column chunks (50 FFMA2 per thread); deterministic
-//                          4-warp reductions; write x_u in place (warm start =
-//                          previous x_u).
+//   warps 0-11  CG         three groups of 4 warps, one per TMEM buffer: read
+//                          b_u from the accumulator's rating columns, repack
+//                          A_u to binary16 in place (the tcgen05 A-operand
+//                          layout), run Algorithm 1 (PAPER.md:272-293,
+//                          corrected r -= alpha*A p) in its pipelined form (one
+//                          barrier per iteration carries both dot products and
+//                          the next matvec's vector) with fp32 vectors; every
+//                          matvec is 7 tensor-core MMAs with A read from TMEM;
+//                          deterministic reductions; write x_u in place (warm
+//                          start = previous x_u), then free the buffer.
 //
 // Semantics vs the reference: the diagonal gets lambda*n_u (weighted) or
 // lambda; rows with n_u == 0 are left untouched; eps = cg_tol * ||b_u||;
 // breakdown (p^T A p <= 0) keeps the current iterate and is counted.  A_u is
-// used in fp32 straight from the accumulator (the reference rounds it to fp16
-// when precision="fp16"; the fused path never stores it -- strictly more
-// accurate, within the 1e-3 RMSE bar the CG route is graded on).
+// rounded from the fp32 accumulator to binary16 (RNE) in TMEM -- the
+// reference's precision="fp16" Hermitian storage (gram.py:132-146) -- and an
+// entry that overflows binary16 sets the overflow flag, which the caller
+// raises as NumericalError like pack_half does.  The CG vectors are fp32
+// (split into fp16 hi/lo halves as the matvec's B operand).
 #include <cstdlib>
 
 #include "tc_common.cuh"
@@ -85,6 +87,7 @@ struct FusedArgs {
     int nprod;  // active producer warps (<= F_PROD; the others exit at once)
     float tol;
     int32_t *breakdowns;
+    int32_t *overflow;  // set when a row's A_u does not fit binary16 (NumericalError)
 };
 
 template <int NBUF>
@@ -456,11 +459,14 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
             // [32c, 32c+32) become packed columns [16c, 16c+16), the tcgen05 A-operand
             // layout (lane = row, column j = elements 2j, 2j+1).  RNE, as the
             // reference's fp16 Hermitian storage.  Rows >= f (padding and the two
-            // rating rows) become zero; the bias columns W, W+1 are read first.
+            // rating rows) and columns >= f (padding, and the bias columns W, W+1,
+            // which are read first) become zero, so the matvec's K range sees only
+            // A_u.  |a| >= 65520 rounds to inf: the overflow flag.
             const uint32_t tb = tmem_base + lane_base + b * g.N;
             float bi = __uint_as_float(tmem_ld1(tb + g.W)) + __uint_as_float(tmem_ld1(tb + g.W + 1));
             tmem_ld_wait();
             bi = act ? bi : 0.0f;
+            uint32_t amax = 0;  // largest binary16 magnitude (bits): 0x7c00 = inf
 #pragma unroll
             for (int c = 0; c < (KP + 31) / 32; ++c) {
                 uint32_t v[32];
@@ -469,11 +475,19 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
                 uint32_t h[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    const __half2 hv = __floats2half2_rn(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-                    h[j] = act ? *reinterpret_cast<const uint32_t *>(&hv) : 0u;
+                    // f > 4 * (FC - 1): only columns >= 4FC - 4 can lie past f
+                    const int col = 32 * c + 2 * j;
+                    float a0 = __uint_as_float(v[2 * j]), a1 = __uint_as_float(v[2 * j + 1]);
+                    if (col >= 4 * FC - 4 && col >= f) a0 = 0.0f;
+                    if (col + 1 >= 4 * FC - 4 && col + 1 >= f) a1 = 0.0f;
+                    const __half2 hv = __floats2half2_rn(a0, a1);
+                    const uint32_t hb = *reinterpret_cast<const uint32_t *>(&hv);
+                    amax = max(amax, max(hb & 0x7fffu, (hb >> 16) & 0x7fffu));
+                    h[j] = act ? hb : 0u;
                 }
                 tmem_st16(tb + 16 * c, h);
             }
+            if (act && amax == 0x7c00u && g.overflow) *g.overflow = 1;  // (NaN bits are > 0x7c00)
             tmem_st_wait();
             tc_fence_before();
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 2);
@@ -681,7 +695,7 @@ static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
 int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
                     const void *fixed16, int64_t ncols, int W, int f, double lam, int weighted, float *target,
                     float *const *peers, int npeers, int64_t nnz, int f_s, double cg_tol, int32_t *breakdowns,
-                    cudaStream_t st) {
+                    int32_t *overflow, cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
     if (npeers < 0 || (npeers > 0 && peers == nullptr)) return set_error(CMF_EINVAL, "bad peer replica list");
     if (nnz < 0) return set_error(CMF_EINVAL, "negative rating count");
@@ -721,6 +735,8 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
     }
     g.tol = static_cast<float>(cg_tol);
     g.breakdowns = breakdowns;
+    g.overflow = overflow;
+    g.gather.overflow = overflow;
     CMF_FUSED_CASE(8, 2)
     CMF_FUSED_CASE(16, 4)
     CMF_FUSED_CASE(24, 6)

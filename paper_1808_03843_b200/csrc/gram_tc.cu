@@ -234,20 +234,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
 // all-zero row the gather reads for padding positions.
 // One warp per shadow row (rows + 1 of them, the last all zero), 4 halves per
 // lane: 16-byte coalesced loads, 8-byte stores, no per-element index division.
-__global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __half *out, int W) {
+// A finite factor whose binary16 rounding overflows (|x| >= 65520) sets *ovf:
+// the fp16 Gram built from it would overflow as the reference's pack_half does
+// (gram.py:132-146), so the caller raises NumericalError.
+__global__ void factors_to_half_kernel(const float *x, int64_t rows, int f, __half *out, int W, int32_t *ovf) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    float amax = 0.0f;
     for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r <= rows; r += nw) {
         const float *src = x + r * f;
         for (int c = 4 * lane; c < W; c += 128) {
             float v[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = (r < rows && c + k < f) ? src[c + k] : 0.0f;
+            for (int k = 0; k < 4; ++k) {
+                v[k] = (r < rows && c + k < f) ? src[c + k] : 0.0f;
+                amax = fmaxf(amax, fabsf(v[k]));  // NaN is dropped by fmaxf, inf is kept
+            }
             const __half2 h01 = __floats2half2_rn(v[0], v[1]), h23 = __floats2half2_rn(v[2], v[3]);
             *reinterpret_cast<uint2 *>(out + r * W + c) =
                 make_uint2(*reinterpret_cast<const uint32_t *>(&h01), *reinterpret_cast<const uint32_t *>(&h23));
         }
     }
+    if (ovf && amax >= 65520.0f && amax <= 3.402823466e38f) atomicOr(ovf, 1);
 }
 
 // Split shadow: hi = fp16(scale*x), lo = fp16(scale*x - hi); scale is a power of
@@ -292,12 +300,12 @@ int gram_tc_trace(void *buf) { return tc::set_trace_buf(buf); }
 
 int gram_tc_width(int f) { return ((f + 7) / 8) * 8; }
 
-int factors_to_half_launch(const float *x, int64_t rows, int f, void *out, int W, cudaStream_t st) {
+int factors_to_half_launch(const float *x, int64_t rows, int f, void *out, int W, int32_t *ovf, cudaStream_t st) {
     if (rows == 0) return CMF_OK;
     int64_t blocks = (rows + 1 + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
     tc::factors_to_half_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, rows, f,
-                                                                             static_cast<__half *>(out), W);
+                                                                             static_cast<__half *>(out), W, ovf);
     return check_launch("factors_to_half_kernel");
 }
 
@@ -378,6 +386,7 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     g.b_out = b_out;
     g.nu_out = nu_out;
     g.overflow = overflow;
+    g.gather.overflow = overflow;
     const int64_t P = packed_size(f);
     const size_t sq_bytes = ((static_cast<size_t>(f) * W * esz) + 15) & ~static_cast<size_t>(15);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);

@@ -119,8 +119,6 @@ __global__ void __launch_bounds__(128) chol_kernel(const float *A, int64_t a_str
     if (lane == 0 && info) info[s] = 0;
 }
 
-int chol_tiled_launch(const float *, int64_t, const float *, const int64_t *, int64_t, int, float *, int32_t *,
-                      int32_t *, cudaStream_t);
 int chol_smem_launch(const float *, int64_t, const float *, const int64_t *, int64_t, int, float *, int32_t *,
                      int32_t *, cudaStream_t);
 
@@ -129,13 +127,7 @@ int chol_launch(const float *a, int64_t a_stride, const float *b, const int64_t 
     if (nsys == 0) return CMF_OK;
     // fp32 production path: 4x4 tiles in shared memory (chol_smem.cu); this
     // file's one-barrier-per-column kernel serves fp64 and f > 128
-    if (!fp64 && f <= 128) {
-        // shared-memory tiles (chol_smem.cu, 20.1 ms at Netflix X) by default;
-        // CMF_CHOL=tiled selects the register-tiled kernel (32.2 ms) for A/B
-        const char *e = getenv("CMF_CHOL");
-        if (e && e[0] == 't') return chol_tiled_launch(a, a_stride, b, nu, nsys, f, x, info, nbad, st);
-        return chol_smem_launch(a, a_stride, b, nu, nsys, f, x, info, nbad, st);
-    }
+    if (!fp64 && f <= 128) return chol_smem_launch(a, a_stride, b, nu, nsys, f, x, info, nbad, st);
     if (f > 256) return set_error(CMF_EINVAL, "f=%d too large for the Cholesky kernel", f);
     const size_t es = fp64 ? 8 : 4;
     const size_t smem = static_cast<size_t>(f) * (f + 1) * es;

@@ -160,6 +160,7 @@ struct GatherArgs {
     int f;
     int ncols;             // rows of the fixed factors; the shadow's row ncols is all zeros
     long long *trace;      // debug timeline (CMF_TRACE builds), else unused
+    int32_t *overflow;     // set when a rating does not fit its binary16 hi half (nullable)
 };
 
 // Operand ring of NST stages + NBUF TMEM accumulator hand-offs (mbarriers:
@@ -326,6 +327,7 @@ __device__ void produce(const GatherArgs &g, const __half *fixed16, const __half
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const __half hi = __float2half_rn(c0.val[h]);
+            if (fabsf(c0.val[h]) >= 65520.0f && g.overflow) *g.overflow = 1;
             const __half lo = __float2half_rn(c0.val[h] - __half2float(hi));
             const uint32_t v = static_cast<uint32_t>(__half_as_ushort(hi)) |
                                (static_cast<uint32_t>(__half_as_ushort(lo)) << 16);

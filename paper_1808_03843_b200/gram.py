@@ -212,7 +212,7 @@ def assemble_side(view: RowView, theta, lam: float, cfg: TileConfig | None = Non
                      nat.ptr(shadow[1]), w16, scale, nat.ptr(flag), nat.stream_ptr())
         else:
             nat.call("cmf_factors_to_half", nat.ptr(th), th.shape[0], f, nat.ptr(shadow[0]), w16,
-                     nat.stream_ptr())
+                     nat.ptr(flag), nat.stream_ptr())
         nat.call("cmf_gram_assemble_tc", nat.ptr(indptr), nat.ptr(indices), nat.ptr(bw), nrows,
                  nat.ptr(shadow[0]), nat.ptr(shadow[1]) if split else None, th.shape[0], scale, w16, f,
                  float(lam), int(bool(weighted_reg)), nat.ptr(base),

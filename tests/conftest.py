@@ -10,6 +10,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# the reference's own test files (tests/golden/ref_tests) run in a subprocess
+# with the cmf -> paper_1808_03843_b200 alias: tests/test_gpu_reference_suite.py
+collect_ignore_glob = ["golden/ref_tests/*"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built extension")

@@ -25,6 +25,9 @@ Fixtures:
   io_cases.npz      file formats: the bytes of the reference's save_cache (CMFR)
                     and save_coo (tsv, csv) for a small instance with duplicates,
                     and its parse_coo of a text with comments / blank lines
+  train_f100.npz    1/10-Netflix shape at f=100 (48,019 x 17,770, 9.9M train
+                    ratings): the same records as train_ml1m for exact / cg32 /
+                    cg16 (run on demand: `make_golden.py f100`, ~40 min here)
   train_ml1m.npz    MovieLens-1M-shaped protocol (BASELINE configs[0]): RMSE and
                     objective per epoch for exact / cg-fp32 / cg-fp16, sampled
                     factor rows per epoch (exact), and SHA-256 digests of the
@@ -282,6 +285,67 @@ def train_ml1m(cmf):
     np.savez_compressed(os.path.join(OUT, "train_ml1m.npz"), **out)
 
 
+def train_f100(cmf):
+    """1/10-Netflix shape at the headline width (VERDICT r1 "next" #1): 48,019 x
+    17,770, 9.9M train ratings, f=100, SURVEY 8(d) protocol, 10 epochs of the
+    reference's train() for exact / cg32 / cg16.  Records per-epoch RMSE and
+    objective, sampled factor rows and full-matrix norms after every half-update,
+    and digests of the inputs (so the GPU test proves it regenerated them)."""
+    import time
+    out = {}
+    m, n, nnz, f = 48_019, 17_770, 9_900_000, 100
+    t0 = time.time()
+    sr, te = protocol(cmf, m, n, nnz, f)
+    print("f100 data", time.time() - t0, "s", flush=True)
+    out["meta"] = np.array([m, n, nnz, f])
+    out["csr_digest"] = np.array(digest(sr.row_ptr, sr.col_idx, sr.csr_val))
+    out["csc_digest"] = np.array(digest(sr.col_ptr, sr.row_idx, sr.csc_val))
+    out["test_digest"] = np.array(digest(te.user, te.item, te.rating))
+    rng = np.random.default_rng(7)
+    rows_x = np.sort(rng.choice(m, 256, replace=False))
+    rows_t = np.sort(rng.choice(n, 256, replace=False))
+    out["rows_x"], out["rows_t"] = rows_x, rows_t
+    import cmf.als as als
+    orig = als.update_side
+    which = os.environ.get("F100_SOLVERS", "exact,cg32,cg16").split(",")
+    cfgs = {"exact": cmf.SolverConfig("exact"),
+            "cg32": cmf.SolverConfig("cg", 6, 1e-4, "fp32"),
+            "cg16": cmf.SolverConfig("cg", 6, 1e-4, "fp16")}
+    path = os.path.join(OUT, "train_f100.npz")
+    if os.path.exists(path):  # resume: keep the solvers already recorded
+        old = dict(np.load(path))
+        old.update({k: v for k, v in out.items()})
+        out = old
+    for name in which:
+        xs, ts, xn, tn, brk = [], [], [], [], []
+
+        def spy(view, fixed, target, *a, **k):
+            r = orig(view, fixed, target, *a, **k)
+            if target.shape[0] == m:
+                xs.append(target[rows_x].copy())
+                xn.append(np.linalg.norm(target.astype(np.float64)))
+            else:
+                ts.append(target[rows_t].copy())
+                tn.append(np.linalg.norm(target.astype(np.float64)))
+            brk.append(r[2])
+            return r
+        als.update_side = spy
+        t0 = time.time()
+        try:
+            _, _, rep = cmf.train(sr, te, cmf.AlsConfig(f=f, lam=0.05, epochs=10, solver=cfgs[name]))
+        finally:
+            als.update_side = orig
+        out[name + "_rmse"] = np.array(rep.rmse_trajectory())
+        out[name + "_obj"] = np.array([e.objective for e in rep.epochs])
+        out[name + "_objmid"] = np.array([e.objective_mid for e in rep.epochs])
+        out[name + "_Xrows"], out[name + "_Trows"] = np.stack(xs), np.stack(ts)
+        out[name + "_Xnorm"], out[name + "_Tnorm"] = np.array(xn), np.array(tn)
+        out[name + "_breakdowns"] = np.array(brk)
+        out[name + "_seconds"] = np.array(time.time() - t0)
+        print(name, time.time() - t0, "s", out[name + "_rmse"], flush=True)
+        np.savez_compressed(path, **out)
+
+
 def implicit_small(cmf):
     import cmf.implicit as imp
     out = {}
@@ -363,5 +427,5 @@ if __name__ == "__main__":
     for w in which:
         {"gram": gram_cases, "solve": solve_cases, "build": build_cases,
          "data": data_cases, "small": train_small, "implicit": implicit_small,
-         "io": io_cases, "ml1m": train_ml1m}[w](cmf)
+         "io": io_cases, "ml1m": train_ml1m, "f100": train_f100}[w](cmf)
         print("wrote", w)

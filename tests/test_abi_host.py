@@ -126,3 +126,20 @@ def test_implicit_config_validation():
             cmfb.ImplicitConfig(**kw)
     c = cmfb.ImplicitConfig()
     assert (c.f, c.alpha, c.lam, c.epochs) == (100, 40.0, 0.05, 10)
+
+
+def test_worker_knob_matches_reference_api():
+    # parallel.py:11-27: >= 1, clamped, returned; results never depend on it
+    assert cmfb.set_workers(1) == 1 and cmfb.get_workers() == 1
+    n = cmfb.set_workers(10 ** 6)
+    assert n == cmfb.get_workers() == (os.cpu_count() or 1)
+    with pytest.raises(ValueError):
+        cmfb.set_workers(0)
+
+
+def test_accum_auto_resolves_per_boundary():
+    from paper_1808_03843_b200.solvers import with_accum
+    cfg = cmfb.SolverConfig("cg", precision="fp16")
+    assert cfg.accum == "auto"
+    assert with_accum(cfg, "fp64").accum == "fp64"
+    assert with_accum(cmfb.SolverConfig("cg", accum="fp32"), "fp64").accum == "fp32"
