@@ -27,9 +27,39 @@ __device__ __forceinline__ double block_reduce_store(double v, double *slot) {
     return v;
 }
 
+// The reference's predict_pairs is numpy's float32 einsum "ij,ij->i"
+// (factors.py:41-54), which this image's numpy runs on its SSE baseline
+// (einsum_sumprod, no FMA): four lanes; each 16-element block adds its four
+// vectors in the order 3, 2, 1, 0; the tail adds zero-padded vectors one at a
+// time; the lanes then reduce as (l0 + l1) + (l2 + l3).  Restating that order
+// with separate round-to-nearest multiplies and adds makes every predicted
+// rating bit-identical to the reference's -- and to the ratings gen_synthetic
+// wrote, so noiseless data round-trips to an RMSE of exactly zero.
 __device__ __forceinline__ float dotf(const float *a, const float *b, int f) {
-    float acc = 0.0f;
-    for (int c = 0; c < f; ++c) acc = fmaf(a[c], b[c], acc);
+    float l0 = 0.0f, l1 = 0.0f, l2 = 0.0f, l3 = 0.0f;
+    int c = 0;
+    for (; c + 16 <= f; c += 16) {
+#pragma unroll
+        for (int k = 12; k >= 0; k -= 4) {
+            l0 = __fadd_rn(__fmul_rn(a[c + k], b[c + k]), l0);
+            l1 = __fadd_rn(__fmul_rn(a[c + k + 1], b[c + k + 1]), l1);
+            l2 = __fadd_rn(__fmul_rn(a[c + k + 2], b[c + k + 2]), l2);
+            l3 = __fadd_rn(__fmul_rn(a[c + k + 3], b[c + k + 3]), l3);
+        }
+    }
+    for (; c < f; c += 4) {
+        l0 = __fadd_rn(__fmul_rn(a[c], b[c]), l0);
+        if (c + 1 < f) l1 = __fadd_rn(__fmul_rn(a[c + 1], b[c + 1]), l1);
+        if (c + 2 < f) l2 = __fadd_rn(__fmul_rn(a[c + 2], b[c + 2]), l2);
+        if (c + 3 < f) l3 = __fadd_rn(__fmul_rn(a[c + 3], b[c + 3]), l3);
+    }
+    return __fadd_rn(__fadd_rn(l0, l1), __fadd_rn(l2, l3));
+}
+
+// als.objective predicts in float64 (als.py:84-87)
+__device__ __forceinline__ double dotd(const float *a, const float *b, int f) {
+    double acc = 0.0;
+    for (int c = 0; c < f; ++c) acc = fma(static_cast<double>(a[c]), static_cast<double>(b[c]), acc);
     return acc;
 }
 
@@ -55,8 +85,8 @@ __global__ void sq_error_csr_kernel(const int64_t *indptr, const int32_t *indice
     for (int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < nrows; u += warps) {
         const float *xu = x + u * f;
         for (int64_t p = indptr[u] + lane; p < indptr[u + 1]; p += 32) {
-            const float pred = dotf(xu, theta + static_cast<int64_t>(indices[p]) * f, f);
-            const double d = static_cast<double>(vals[p]) - static_cast<double>(pred);
+            const double pred = dotd(xu, theta + static_cast<int64_t>(indices[p]) * f, f);
+            const double d = static_cast<double>(vals[p]) - pred;
             acc = fma(d, d, acc);
         }
     }

@@ -27,6 +27,7 @@ exactly (tests/test_distributed.py).
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -55,6 +56,69 @@ def shard_view(indptr, indices, values, lo: int, hi: int):
     p1 = int(indptr[hi])
     ptr = indptr[lo:hi + 1] - p0
     return ptr, indices[p0:p1], values[p0:p1]
+
+
+@dataclass
+class ShardedRatings:
+    """One rank's byte-exact slices of the CSR (user rows [xb[r], xb[r+1])) and
+    CSC (item rows [tb[r], tb[r+1])) arrays, pointers rebased; m, n, nnz are the
+    global sizes.  Built by ``shard_ratings`` without materialising the other
+    ranks' rows on this device."""
+
+    m: int
+    n: int
+    nnz: int
+    xb: list
+    tb: list
+    x_view: tuple
+    t_view: tuple
+
+
+def shard_ratings(triples, m: int, n: int, rank: int, world: int) -> ShardedRatings:
+    """Per-rank build: the row/column counts of the host triples
+    give the nnz-balanced boundaries (every rank computes the same ones); the
+    rank then builds on its device only the triples of its user range (its CSR
+    rows) and of its item range (its CSC rows).  Duplicates of a (user, item)
+    pair fall in the same shard, so the last-wins de-duplication of
+    data.build (data.py:205-249) is shard-local and the concatenated shards
+    equal the single-device arrays byte for byte (tests/test_distributed.py).
+    The boundaries balance the pre-de-duplication counts, which equal the
+    final ones whenever the triples are distinct (the synthetic generator)."""
+    from .data import Triples, build_device
+    u = np.asarray(triples.user.cpu() if isinstance(triples.user, torch.Tensor) else triples.user)
+    v = np.asarray(triples.item.cpu() if isinstance(triples.item, torch.Tensor) else triples.item)
+    r = np.asarray(triples.rating.cpu() if isinstance(triples.rating, torch.Tensor) else triples.rating)
+    if len(u) and (u.min() < 0 or u.max() >= m or v.min() < 0 or v.max() >= n):
+        raise DataError(f"triple out of range for a {m}x{n} matrix")
+    row_ptr = np.zeros(m + 1, np.int64)
+    np.cumsum(np.bincount(u, minlength=m), out=row_ptr[1:])
+    col_ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(v, minlength=n), out=col_ptr[1:])
+    xb, tb = shard_bounds(row_ptr, world), shard_bounds(col_ptr, world)
+    xlo, xhi, tlo, thi = xb[rank], xb[rank + 1], tb[rank], tb[rank + 1]
+    if world == 1:
+        full = build_device(Triples(u, v, r), m, n)
+        return ShardedRatings(m, n, full.nnz, xb, tb,
+                              (full.row_ptr, full.col_idx, full.csr_val),
+                              (full.col_ptr, full.row_idx, full.csc_val))
+    sel = np.flatnonzero((u >= xlo) & (u < xhi))
+    part = build_device(Triples(u[sel] - xlo, v[sel], r[sel]), xhi - xlo, n)
+    x_view = (part.row_ptr, part.col_idx, part.csr_val)
+    nnz_x = part.nnz
+    del part
+    sel = np.flatnonzero((v >= tlo) & (v < thi))
+    part = build_device(Triples(u[sel], v[sel] - tlo, r[sel]), m, thi - tlo)
+    t_view = (part.col_ptr, part.row_idx, part.csc_val)
+    del part
+    # global nnz after de-duplication = sum of every rank's CSR shard
+    nnz = nnz_x
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        t = torch.tensor([nnz_x], dtype=torch.int64,
+                         device=x_view[0].device if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t)
+        nnz = int(t.item())
+    return ShardedRatings(m, n, nnz, xb, tb, x_view, t_view)
 
 
 class RowGather:
@@ -101,14 +165,24 @@ class ShardedALS:
         self.weighted_reg = weighted_reg
         self.rank, self.world, self.group = rank, world, group
         self.gram_kernel = resolve_gram_kernel(gram_kernel, solver, f)
-        dev = ratings.row_ptr.device
         self.m, self.n = ratings.m, ratings.n
-        self.xb = shard_bounds(ratings.row_ptr, world)
-        self.tb = shard_bounds(ratings.col_ptr, world)
+        if isinstance(ratings, ShardedRatings):
+            # built per rank (shard_ratings): only this rank's rows are resident
+            if len(ratings.xb) != world + 1:
+                raise DataError(f"shards were built for {len(ratings.xb) - 1} ranks, not {world}")
+            self.xb, self.tb = ratings.xb, ratings.tb
+            self.x_view, self.t_view = ratings.x_view, ratings.t_view
+            dev = self.x_view[0].device
+        else:
+            dev = ratings.row_ptr.device
+            self.xb = shard_bounds(ratings.row_ptr, world)
+            self.tb = shard_bounds(ratings.col_ptr, world)
+            self.x_view = shard_view(ratings.row_ptr, ratings.col_idx, ratings.csr_val,
+                                     self.xb[rank], self.xb[rank + 1])
+            self.t_view = shard_view(ratings.col_ptr, ratings.row_idx, ratings.csc_val,
+                                     self.tb[rank], self.tb[rank + 1])
         xs = (self.xb[rank], self.xb[rank + 1])
         ts = (self.tb[rank], self.tb[rank + 1])
-        self.x_view = shard_view(ratings.row_ptr, ratings.col_idx, ratings.csr_val, *xs)
-        self.t_view = shard_view(ratings.col_ptr, ratings.row_idx, ratings.csc_val, *ts)
         self.x_plan = HalfUpdatePlan(xs[1] - xs[0], f, solver, dev)
         self.t_plan = HalfUpdatePlan(ts[1] - ts[0], f, solver, dev)
         if world > 1:

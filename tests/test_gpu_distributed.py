@@ -25,12 +25,17 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(rank, world, solver, peer=False):
+def _run(rank, world, solver, peer=False, per_rank=False):
     import paper_1808_03843_b200 as cmfb
-    from paper_1808_03843_b200.distributed import ShardedALS
+    from paper_1808_03843_b200.distributed import ShardedALS, shard_ratings
     torch.cuda.set_device(0)
     m, n, nnz = SHAPE
-    train, _ = cmfb.gen_synthetic_device(m, n, F, nnz, 0.1, 0.1, seed=3)
+    if per_rank:
+        # reference protocol on the host, each rank builds only its shards
+        t, _ = cmfb.gen_synthetic(m, n, F, nnz / (m * n), 0.1, 3)
+        train = shard_ratings(t, m, n, rank, world)
+    else:
+        train, _ = cmfb.gen_synthetic_device(m, n, F, nnz, 0.1, 0.1, seed=3)
     x = torch.from_numpy(cmfb.init_factors(m, F, 0.1, [0, 0])).cuda()
     th = torch.from_numpy(cmfb.init_factors(n, F, 0.1, [0, 1])).cuda()
     method, prec = {"cg16": ("cg", "fp16"), "exact": ("exact", "fp32")}[solver]
@@ -48,28 +53,57 @@ def _run(rank, world, solver, peer=False):
     return out
 
 
-def _worker(rank, world, port, out, solver, peer=False):
+def _worker(rank, world, port, out, solver, peer=False, per_rank=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        x, th, rows = _run(rank, world, solver, peer)
+        x, th, rows = _run(rank, world, solver, peer, per_rank)
         np.savez(f"{out}_{rank}.npz", x=x, th=th, xr=rows["x"], tr=rows["t"])
         dist.barrier()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("solver,peer", [("cg16", False), ("exact", False), ("cg16", True)])
-def test_two_rank_engine_equals_single_rank(tmp_path, solver, peer):
+@pytest.mark.parametrize("solver,peer,per_rank", [("cg16", False, False), ("exact", False, False),
+                                                  ("cg16", True, False), ("cg16", True, True)])
+def test_two_rank_engine_equals_single_rank(tmp_path, solver, peer, per_rank):
     """peer=True: the fused kernel stores each solved row into the other rank's
     replica through a CUDA-IPC mapping (cmf_fused_cg_update_peers) instead of
-    an all-gather."""
+    an all-gather.  per_rank=True: each rank builds only its own shards from the
+    host triples (distributed.shard_ratings)."""
     out = str(tmp_path / "r")
-    mp.spawn(_worker, args=(2, _free_port(), out, solver, peer), nprocs=2, join=True)
-    x1, th1, _ = _run(0, 1, solver)
+    mp.spawn(_worker, args=(2, _free_port(), out, solver, peer, per_rank), nprocs=2, join=True)
+    x1, th1, _ = _run(0, 1, solver, per_rank=per_rank)
     parts = [np.load(f"{out}_{r}.npz") for r in range(2)]
     assert parts[0]["xr"] > 0 and parts[1]["xr"] > 0  # both ranks solved rows
     for p in parts:  # every rank holds the full, identical factors
         assert np.array_equal(p["x"], x1)
         assert np.array_equal(p["th"], th1)
+
+
+def test_per_rank_shards_concatenate_to_build(cuda_device):
+    """shard_ratings for k ranks: the CSR / CSC slices each rank builds on its
+    own concatenate to the single-device build byte for byte (incl. duplicate
+    triples, last wins, and empty rows)."""
+    import paper_1808_03843_b200 as cmfb
+    from paper_1808_03843_b200.distributed import shard_ratings
+    rng = np.random.default_rng(11)
+    m, n, k = 500, 300, 20_000
+    u = rng.integers(0, m - 3, k)
+    v = rng.integers(0, n, k)
+    t = cmfb.Triples(u, v, rng.standard_normal(k).astype(np.float32))
+    full = cmfb.build(t, m, n)
+    for world in (1, 2, 3, 5):
+        parts = [shard_ratings(t, m, n, r, world) for r in range(world)]
+        for side, ref in (("x_view", (full.row_ptr, full.col_idx, full.csr_val)),
+                          ("t_view", (full.col_ptr, full.row_idx, full.csc_val))):
+            ptrs, idxs, vals = [], [], []
+            for p in parts:
+                ptr, idx, val = (a.cpu().numpy() for a in getattr(p, side))
+                ptrs.append(ptr[1:] + (ptrs[-1][-1] if ptrs else 0))
+                idxs.append(idx)
+                vals.append(val)
+            assert np.array_equal(np.concatenate([[0]] + ptrs), ref[0])
+            assert np.array_equal(np.concatenate(idxs), ref[1])
+            assert np.array_equal(np.concatenate(vals).view(np.uint32), ref[2].view(np.uint32))

@@ -95,20 +95,25 @@ def test_tc_train_rmse_trajectory_ml1m(golden, cuda_device):
     t, _ = cmfb.gen_synthetic(m, n, f, round(nnz / 0.9) / (m * n), 0.1, 0)
     tr, te = cmfb.split_holdout(t, 0.1, 1)
     sr = cmfb.build(tr, m, n)
-    for solver, prec in (("cg16", "fp16"), ("cg32", "fp32")):
-        cfg = cmfb.AlsConfig(f=f, lam=0.05, epochs=10, gram_kernel="tc",
+    # cg16 runs the fused tcgen05 kernel; precision="fp32" keeps fp32 Hermitian
+    # storage and therefore takes the split-precision two-step route
+    for solver, prec, kern in (("cg16", "fp16", "tc"), ("cg32", "fp32", "auto")):
+        cfg = cmfb.AlsConfig(f=f, lam=0.05, epochs=10, gram_kernel=kern,
                              solver=cmfb.SolverConfig("cg", precision=prec))
         _, _, rep = cmfb.train(sr, te, cfg)
         traj = np.array(rep.rmse_trajectory())
         assert np.abs(traj - g[solver + "_rmse"]).max() < 1e-3, (solver, traj)
 
 
-def test_fused_tc_cg_matches_two_step(cuda_device):
+def test_fused_tc_cg_matches_two_step(cuda_device, monkeypatch):
     """update_side with the fused kernel (Gram in TMEM -> CG in registers) vs the
     two-step tensor-core path (packed fp32 A_u in HBM -> batched CG kernel):
     same fp16 Gram operands, same CG recurrence, so the solutions agree to fp32
     rounding; rows without ratings are untouched in both."""
     import torch
+    # both routes store A_u in binary16 from the same fp32 accumulator; the
+    # two-step solver then runs the same pipelined recurrence as the fused one
+    monkeypatch.setenv("CMF_CG_PIPELINED", "1")
     for f, (m, n, nnz) in ((100, (300, 900, 30000)), (32, (500, 200, 8000)), (8, (50, 40, 300))):
         t, _ = cmfb.gen_synthetic(m, n, f, nnz / (m * n), 0.1, 3)
         sr = cmfb.build(t, m + 1, n)  # last user has no ratings
@@ -117,7 +122,7 @@ def test_fused_tc_cg_matches_two_step(cuda_device):
         for kern in ("tc", "tc_unfused"):
             x = cmfb.init_factors(m + 1, f, 0.1, [0, 0])
             cmfb.update_side(sr.csr_view(), theta, x, 0.05,
-                             cmfb.SolverConfig("cg", precision="fp32"), gram_kernel=kern)
+                             cmfb.SolverConfig("cg", precision="fp16"), gram_kernel=kern)
             outs.append(x)
         x0 = cmfb.init_factors(m + 1, f, 0.1, [0, 0])
         assert np.array_equal(outs[0][m], x0[m]) and np.array_equal(outs[1][m], x0[m])
@@ -125,10 +130,11 @@ def test_fused_tc_cg_matches_two_step(cuda_device):
         assert rel < 1e-4, (f, rel)
 
 
-def test_fused_tc_cg_shapes_match_two_step(cuda_device):
+def test_fused_tc_cg_shapes_match_two_step(cuda_device, monkeypatch):
     """The fused kernel's other CTA shapes against the two-step path: two CG
     groups for f > 104, and the gather-heavy shape for views whose rows average
     >= 1024 ratings (the item side of a tall matrix)."""
+    monkeypatch.setenv("CMF_CG_PIPELINED", "1")
     for f, (m, n, nnz), side in ((120, (400, 300, 24000), "csr"), (112, (300, 500, 20000), "csr"),
                                  (100, (6000, 40, 120000), "csc"), (24, (5000, 30, 90000), "csc")):
         t, _ = cmfb.gen_synthetic(m, n, f, nnz / (m * n), 0.1, 5)
@@ -141,15 +147,16 @@ def test_fused_tc_cg_shapes_match_two_step(cuda_device):
         outs = []
         for kern in ("tc", "tc_unfused"):
             x = cmfb.init_factors(rows, f, 0.1, [0, 0])
-            cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp32"), gram_kernel=kern)
+            cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp16"), gram_kernel=kern)
             outs.append(x)
         rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1])
         assert rel < 1e-4, (f, side, rel)
 
 
-def test_fused_tc_cg_large_fixed_side(cuda_device):
+def test_fused_tc_cg_large_fixed_side(cuda_device, monkeypatch):
     """Short rows over a fixed side too large for L2 residency (> 32 MB of
     binary16 shadow): the fused kernel runs all 7 gather warps there."""
+    monkeypatch.setenv("CMF_CG_PIPELINED", "1")
     import torch
     f = 100
     train, _ = cmfb.gen_synthetic_device(2000, 170_000, f, 100_000, 0.1, 0.1, seed=2)
@@ -159,7 +166,7 @@ def test_fused_tc_cg_large_fixed_side(cuda_device):
     outs = []
     for kern in ("tc", "tc_unfused"):
         x = torch.from_numpy(cmfb.init_factors(2000, f, 0.1, [0, 0])).cuda()
-        cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp32"), gram_kernel=kern)
+        cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp16"), gram_kernel=kern)
         outs.append(x)
     rel = float(torch.linalg.norm(outs[0] - outs[1]) / torch.linalg.norm(outs[1]))
     assert rel < 1e-4, rel
