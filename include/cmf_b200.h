@@ -144,6 +144,23 @@ int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, con
                               int32_t f, double lam, int32_t weighted_reg, float *target,
                               float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
                               int32_t *breakdowns, int32_t *overflow_flag, void *stream);
+/*
+ * cmf_fused_cg_update_peers with a caller-supplied device workspace: for long
+ * rows (avg >= 1024 ratings) over a fixed side whose binary16 shadow exceeds
+ * L2 (> 48 MB), the half-update runs as two passes over the fixed side's row
+ * range (first half of the column ids, then the second half), parking each
+ * row's fp32 partial Gram in the workspace, so each pass's gather stays
+ * L2-resident.  Same results up to fp32 summation order.  The workspace must
+ * hold cmf_fused_cg_workspace_bytes(nrows, f) bytes (256-byte aligned); with
+ * less (or NULL) the single pass runs.  CMF_TWO_PASS=0/1 forces the choice.
+ */
+int cmf_fused_cg_update_ws(const int64_t *indptr, const int32_t *indices, const float *values,
+                           int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
+                           int32_t f, double lam, int32_t weighted_reg, float *target,
+                           float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
+                           int32_t *breakdowns, int32_t *overflow_flag, void *workspace,
+                           int64_t workspace_bytes, void *stream);
+int64_t cmf_fused_cg_workspace_bytes(int64_t nrows, int32_t f);
 /* CUDA IPC for the peer replicas: export a device pointer (any address inside
  * an allocation) as a 64-byte handle + offset; open it in another process
  * (peer access enabled lazily over NVLink); close with the same offset. */

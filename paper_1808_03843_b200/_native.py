@@ -48,6 +48,9 @@ _SIGNATURES = {
                                            _i32, _f64, _vp, _vp, _vp]),
     "cmf_fused_cg_update_peers": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp,
                                                  _vp, _i32, _i32, _f64, _vp, _vp, _vp]),
+    "cmf_fused_cg_update_ws": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32,
+                                              _vp, _vp, _i32, _i32, _f64, _vp, _vp, _vp, _i64, _vp]),
+    "cmf_fused_cg_workspace_bytes": (ctypes.c_int64, [_i64, _i32]),
     "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp]),
     "cmf_spmm_bias": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),
     "cmf_batch_cg": (ctypes.c_int, [_vp, _i32, _i64, _vp, _vp, _vp, _f64, _vp, _i64, _i32, _i32,
@@ -79,6 +82,11 @@ def load_library(path: str = LIB_PATH):
                 raise CmfError(f"native library missing: {path} (run __graft_entry__.build())")
             L = ctypes.CDLL(path)
             for name, (res, args) in _SIGNATURES.items():
+                # an older build (A/B timing via CMF_LIB_PATH) may lack newer entry
+                # points; they fail when called (tests/test_abi_host.py checks that
+                # the current build exports every one)
+                if not hasattr(L, name):
+                    continue
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
@@ -111,7 +119,7 @@ def check(rc: int, what: str = ""):
 
 # Kernel-launching entry points called since the counter was last reset (the
 # benchmark's "gpu_launches" claim counts launches of OUR kernels).
-_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
+_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_fused_cg_update_ws": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
                 "cmf_batch_cholesky": 1, "cmf_pack_half": 1, "cmf_sq_error": 2,
                 "cmf_sq_error_csr": 2, "cmf_weighted_sqnorm": 2, "cmf_predict_pairs": 1}
 LAUNCHES = [0]

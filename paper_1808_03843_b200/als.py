@@ -114,8 +114,8 @@ class _Workspace:
     def __init__(self):
         self.bufs = {}
 
-    def get(self, dev, nbytes: int) -> torch.Tensor:
-        key = (dev.index,)
+    def get(self, dev, nbytes: int, key: str = "systems") -> torch.Tensor:
+        key = (dev.index, key)
         t = self.bufs.get(key)
         if t is None or t.numel() < nbytes:
             self.bufs.pop(key, None)
@@ -220,12 +220,18 @@ class HalfUpdatePlan:
                       nat.ptr(tg) + 4 * row0 * f)
             tail = (int(solver.cg_iters), float(solver.cg_tol), nat.ptr(self.flags) + 4,
                     nat.ptr(self.flags), st)
-            if peers is not None and peers.numel():
-                if row0:
-                    raise DataError("peer stores take whole views (row0 == 0)")
-                nat.call("cmf_fused_cg_update_peers", *common, nat.ptr(peers), int(peers.numel()), *tail)
-            else:
-                nat.call("cmf_fused_cg_update", *common, *tail)
+            if peers is not None and peers.numel() and row0:
+                raise DataError("peer stores take whole views (row0 == 0)")
+            npeers = int(peers.numel()) if peers is not None else 0
+            # long rows over a fixed side larger than L2: the kernel runs two passes
+            # and parks each row's partial Gram in this workspace (~1 GB for the
+            # Netflix item side); other views never touch it
+            ws, wsb = None, 0
+            if nnz >= 1024 * max(nrows, 1) and fx.shape[0] * self.w16 * 2 > (48 << 20):
+                wsb = int(nat.lib().cmf_fused_cg_workspace_bytes(nrows, f))
+                ws = _WS.get(self.dev, wsb, key="fused2p")
+            nat.call("cmf_fused_cg_update_ws", *common, nat.ptr(peers) if npeers else None, npeers,
+                     tail[0], tail[1], tail[2], tail[3], nat.ptr(ws), wsb, tail[4])
             if record is not None:
                 e1.record()
                 record.setdefault("fused_tc_cg", []).append((e0, e1))

@@ -27,7 +27,9 @@ int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, con
 int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, int, float, int32_t *, cudaStream_t);
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
-                    int, float *, float *const *, int, int64_t, int, double, int32_t *, int32_t *, cudaStream_t);
+                    int, float *, float *const *, int, int64_t, int, double, int32_t *, int32_t *, void *, int64_t,
+                    cudaStream_t);
+int64_t fused_cg_workspace_bytes(int64_t nrows, int W);
 int factors_to_half_launch(const float *, int64_t, int, void *, int, int32_t *, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
                      float *, cudaStream_t);
@@ -201,7 +203,7 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
     REQUIRE(indptr && fixed16 && target, "null argument");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, nullptr,
-                           0, nnz, f_s, cg_tol, breakdowns, overflow_flag, S(stream));
+                           0, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, S(stream));
 }
 
 int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, const float *values,
@@ -218,7 +220,33 @@ int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, con
     REQUIRE(npeers == 0 || peer_targets, "null peer list");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
-                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, S(stream));
+                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, S(stream));
+}
+
+int cmf_fused_cg_update_ws(const int64_t *indptr, const int32_t *indices, const float *values,
+                           int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
+                           int32_t f, double lam, int32_t weighted_reg, float *target,
+                           float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
+                           int32_t *breakdowns, int32_t *overflow_flag, void *workspace,
+                           int64_t workspace_bytes, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(f_s >= 1, "cg_iters must be >= 1");
+    REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
+    REQUIRE(npeers >= 0 && npeers <= 64, "npeers must be in [0, 64]");
+    REQUIRE(workspace_bytes >= 0, "negative workspace size");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && fixed16 && target, "null argument");
+    REQUIRE(npeers == 0 || peer_targets, "null peer list");
+    REQUIRE(ncols >= 1, "ncols must be >= 1");
+    REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 255) == 0, "workspace must be 256-byte aligned");
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
+                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, workspace,
+                           workspace_bytes, S(stream));
+}
+
+int64_t cmf_fused_cg_workspace_bytes(int64_t nrows, int32_t f) {
+    if (nrows < 0 || f < 1) return 0;
+    return fused_cg_workspace_bytes(nrows, gram_tc_width(f));
 }
 
 int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_weights,

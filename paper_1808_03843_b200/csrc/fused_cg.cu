@@ -39,7 +39,13 @@
 namespace cmf {
 namespace tc {
 
-constexpr int F_PROD = 7;  // producer warps: the gather rate scales with issuing warps
+// producer warps: the gather rate scales with issuing warps.  Short rows (the
+// user side) share the SM with 4 CG groups and run 7; long rows (the item side)
+// leave the 2 CG groups mostly idle and run 11.  (A producer waits on stage
+// it's slot for the release of stage it - NST, which is unambiguous only while
+// producers <= ring stages: 12.)
+constexpr int F_PROD_SHORT = 7;
+constexpr int F_PROD_LONG = 11;
 constexpr int CG_THREADS = 128;
 constexpr int MVB_OPERAND = 4096;  // matvec B operand: 16 rows x 128 halves, K-major SW128 (2 K-atoms)
 constexpr int MVB_BYTES = 5120;    // + warp partials, 1024-aligned per group
@@ -52,16 +58,31 @@ constexpr int MVB_BYTES = 5120;    // + warp partials, 1024-aligned per group
 // dominates and CG is rare, and two CG groups leave the producers more of the
 // SM (measured: Theta side 3.21 -> 3.03 ms at Netflix shape).
 constexpr int LONG_ROW_NNZ = 1024;
+// TMEM plan (512 columns): NBUF fp32 Gram accumulators of N <= NMAX columns
+// each, then one binary16 A_u slot of KP/2 columns per CG group, then one
+// 16-column matvec result block per group.  A group copies its row's A_u out
+// of the accumulator (repacking to binary16) and frees the accumulator at once,
+// so the MMA warp builds the next Grams while up to NG systems are in CG.
 template <int FC, bool LONG = false>
 struct FusedShape {
-    static constexpr int NG = (FC <= 26 && !LONG) ? 3 : 2;
-    static constexpr int NBUF = NG + 1;  // TMEM accumulators rotate over the NG groups
-    static constexpr int THREADS = 32 * (4 * NG + F_PROD + 1);
-    static constexpr int MMA_WARP = 4 * NG + F_PROD;
-    static constexpr int LAUNCH_REGS = NG == 3 ? 96 : 128;
-    static constexpr int CG_REGS = NG == 3 ? 112 : 168;
-    static constexpr int AUX_REGS = NG == 3 ? 72 : 88;
-    static_assert(NG * 128 * CG_REGS + 256 * AUX_REGS == THREADS * LAUNCH_REGS, "register budget");
+    static constexpr int KP = (FC * 4 + 15) / 16 * 16;         // matvec K extent
+    static constexpr int SLOT = KP / 2;                         // packed binary16 A_u columns
+    static constexpr int NMAX = ((FC * 4 + 7) / 8 * 8 + 2 + 15) / 16 * 16;  // accumulator width bound
+    static constexpr int NG = (FC <= 26 && !LONG) ? 4 : 2;
+    static constexpr int tmem_need(int nbuf) { return (nbuf * NMAX + NG * SLOT + 15) / 16 * 16 + 16 * NG; }
+    static constexpr int NBUF = (LONG && tmem_need(3) <= 512) ? 3 : 2;
+    static constexpr int NPROD = LONG ? F_PROD_LONG : F_PROD_SHORT;
+    static constexpr int THREADS = 32 * (4 * NG + NPROD + 1);
+    static constexpr int MMA_WARP = 4 * NG + NPROD;
+    // 768 threads (4 CG groups + 7 producers), 640 (2 groups + 11 producers) or
+    // 512 (2 groups + 7, f > 104 short rows): registers per thread at launch
+    static constexpr int LAUNCH_REGS = THREADS == 768 ? 80 : (THREADS == 640 ? 96 : 128);
+    static constexpr int CG_REGS = NG == 4 ? 88 : (THREADS == 640 ? 144 : 168);
+    static constexpr int AUX_REGS = THREADS == 512 ? 88 : 64;
+    static_assert(THREADS == 768 || THREADS == 640 || THREADS == 512, "CTA shape");
+    static_assert(NPROD <= 12, "producers <= ring stages");
+    static_assert(NG * 128 * CG_REGS + 32 * (NPROD + 1) * AUX_REGS <= THREADS * LAUNCH_REGS, "register budget");
+    static_assert(tmem_need(NBUF) <= 512, "TMEM plan");
 };
 
 template <int R>
@@ -77,17 +98,23 @@ struct FusedArgs {
     GatherArgs gather;
     const __half *fixed16;  // binary16 shadow of the fixed factors (ncols, W)
     int W, N, tmem_cols;  // shadow width, accumulator width (Gram + rating columns W, W+1)
-    int dmv_tail, dmv_off;  // matvec result columns: after the NBUF buffers, or inside each buffer
+    int slot_base, dmv_base;  // TMEM columns of the A_u slots and the matvec result blocks
     double lam;
     int weighted;
     float *target;  // (nrows, f) in/out
     float *const *peers;  // device array of npeers replicas of target (rows at the same index), or null
     int npeers;
     int f_s;
-    int nprod;  // active producer warps (<= F_PROD; the others exit at once)
+    int nprod;  // active producer warps (<= the shape's NPROD; the others exit at once; <= 0: all)
     float tol;
     int32_t *breakdowns;
     int32_t *overflow;  // set when a row's A_u does not fit binary16 (NumericalError)
+    // Two-pass Gram (gather.pass 1 / 2, long rows over a fixed side larger than
+    // L2 can hold): pass 1 stores each row's partial accumulator (columns
+    // [0, W+2): the first-segment Gram and bias) at partial + (u*128 + i)*PWS
+    // for lanes i < f; pass 2 adds it to the second segment's accumulator.
+    float *partial;
+    int pws;  // partial row stride in floats (roundup4(W + 2))
 };
 
 template <int NBUF>
@@ -396,6 +423,12 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
     using PipeT = FPipe<NBUF>;
     constexpr int KP = (FC * 4 + 15) / 16 * 16;  // matvec K extent (>= f), 16-half MMA steps
     constexpr int F_STAGES = PipeT::kStages;
+    // "Gram ready" hand-off without parity aliasing: a waiter must never be two
+    // phases behind its barrier.  With NG >= NBUF the row a group waits for can
+    // be two phases ahead on its buffer's barrier but not on a per-group barrier
+    // (row r + NG needs a buffer that row r's group releases); with NG < NBUF the
+    // reverse holds (rows <= r - NG are committed before row r's group waits).
+    constexpr bool kGroupFull = F_GROUPS >= NBUF;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const GatherArgs &ga = g.gather;
     const int f = ga.f;
@@ -405,7 +438,8 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
     unsigned char *scratch = smem + F_STAGES * PipeT::kStageBytes;
     uint64_t *bars = reinterpret_cast<uint64_t *>(scratch + F_GROUPS * MVB_BYTES);
     uint64_t *mvbars = bars + PipeT::kBars;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mvbars + F_GROUPS);
+    uint64_t *gfull = mvbars + F_GROUPS;  // per-group "Gram ready" (row r -> group r % NG)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gfull + F_GROUPS);
     PipeT pp{smem_u32(smem), smem_u32(bars)};
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -413,7 +447,10 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
     for (int i = tid; i < F_GROUPS * MVB_BYTES / 16; i += F_THREADS)
         reinterpret_cast<int4 *>(scratch)[i] = make_int4(0, 0, 0, 0);
     if (tid == 0) {
-        for (int q = 0; q < F_GROUPS; ++q) mbar_init(smem_u32(mvbars + q), 1);
+        for (int q = 0; q < F_GROUPS; ++q) {
+            mbar_init(smem_u32(mvbars + q), 1);
+            mbar_init(smem_u32(gfull + q), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == F_MMA_WARP) tmem_alloc(smem_u32(tmem_slot), g.tmem_cols);
@@ -431,7 +468,8 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
                                            blockIdx.x, G);
     } else if (warp == F_MMA_WARP) {
         regs_dec<Shape::AUX_REGS>();
-        issue_mma<F_STAGES, false, NBUF>(ga, pp, tmem_base, g.N, blockIdx.x, G);
+        issue_mma<F_STAGES, false, NBUF>(ga, pp, tmem_base, g.N, blockIdx.x, G, smem_u32(gfull),
+                                         kGroupFull ? F_GROUPS : 0);
     } else {
         regs_inc<Shape::CG_REGS>();
         // ------------------------------------------------------------ CG groups
@@ -452,56 +490,121 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
             float* const tgt = g.target + u * f;
             float xi = act ? tgt[i] : 0.0f;  // warm start, loaded while the Gram is built
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 0);
-            mbar_wait_backoff<64, 4096>(pp.tfull(b), (r_here / NBUF) & 1);  // long rows keep the group idle
+            // long rows keep the group idle: back-off wait
+            if (ga.pass == 2 && act) {  // the first segment's partial: into L2 while the Gram builds
+                const char *pr = reinterpret_cast<const char *>(g.partial + (u * 128 + i) * g.pws);
+                for (int o = 0; o < g.pws * 4; o += 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr + o));
+            }
+            if (kGroupFull)
+                mbar_wait_backoff<64, 4096>(smem_u32(gfull + grp), (r_here / F_GROUPS) & 1);
+            else
+                mbar_wait_backoff<64, 4096>(pp.tfull(b), (r_here / NBUF) & 1);
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 1);
             tc_fence_after();
-            // A_u (fp32, thread i <-> lane i <-> row i) -> binary16 in place: columns
-            // [32c, 32c+32) become packed columns [16c, 16c+16), the tcgen05 A-operand
-            // layout (lane = row, column j = elements 2j, 2j+1).  RNE, as the
-            // reference's fp16 Hermitian storage.  Rows >= f (padding and the two
-            // rating rows) and columns >= f (padding, and the bias columns W, W+1,
-            // which are read first) become zero, so the matvec's K range sees only
-            // A_u.  |a| >= 65520 rounds to inf: the overflow flag.
+            // A_u (fp32, thread i <-> lane i <-> row i) -> binary16 in this group's
+            // slot: accumulator columns [32c, 32c+32) become slot columns
+            // [16c, 16c+16), the tcgen05 A-operand layout (lane = row, column j =
+            // elements 2j, 2j+1).  RNE, as the reference's fp16 Hermitian storage.
+            // Columns >= f (padding, and the rating columns W, W+1) become zero, so
+            // the matvec's K range sees only A_u; rows >= f keep whatever they hold
+            // (a D row depends only on its own A row, and rows >= f are never
+            // read).  |a| >= 65520 rounds to inf: the overflow flag.  The
+            // accumulator is released as soon as it has been read.
             const uint32_t tb = tmem_base + lane_base + b * g.N;
-            float bi = __uint_as_float(tmem_ld1(tb + g.W)) + __uint_as_float(tmem_ld1(tb + g.W + 1));
-            tmem_ld_wait();
+            // segmented passes: which parts hold data (the MMA skipped an empty segment)
+            bool seg_acc = true, seg_part = false;
+            if (ga.pass) {
+                const int64_t sp = ga.seg[u];
+                seg_acc = ga.pass == 1 ? sp > p0 : ga.indptr[u + 1] > sp;
+                seg_part = ga.pass == 2 && sp > p0;
+            }
+            float *const prow = g.partial + (u * 128 + i) * g.pws;
+            if (ga.pass == 1) {
+                // first segment: park the fp32 accumulator (Gram + bias columns) in HBM
+                if (seg_acc) {
+#pragma unroll 1
+                    for (int c = 0; c < g.W + 2; c += 16) {
+                        uint32_t v[16];
+                        tmem_ldn<16>(tb + c, v);
+                        tmem_ld_wait();
+                        if (act) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                if (c + j < g.pws)
+                                    *reinterpret_cast<float4 *>(prow + c + j) =
+                                        make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                    __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(pp.tempty(b));
+                continue;
+            }
+            float bi = 0.0f;
+            if (seg_acc) {
+                bi = __uint_as_float(tmem_ld1(tb + g.W)) + __uint_as_float(tmem_ld1(tb + g.W + 1));
+                tmem_ld_wait();
+            }
+            if (seg_part && act) bi += prow[g.W] + prow[g.W + 1];
             bi = act ? bi : 0.0f;
-            uint32_t amax = 0;  // largest binary16 magnitude (bits): 0x7c00 = inf
+            const uint32_t a_tmem = tmem_base + g.slot_base + grp * Shape::SLOT;
+            float amax = 0.0f;
 #pragma unroll
             for (int c = 0; c < (KP + 31) / 32; ++c) {
-                uint32_t v[32];
-                tmem_ldn<32>(tb + 32 * c, v);
-                tmem_ld_wait();
-                uint32_t h[16];
+                uint32_t v[32], h[16];
+                if (seg_acc) {
+                    if (32 * c + 32 <= KP) tmem_ldn<32>(tb + 32 * c, v);
+                    else tmem_ldn<16>(tb + 32 * c, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0u;
+                }
+                if (seg_part && act) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        if (32 * c + j >= KP) break;
+                        if (32 * c + j < g.pws) {
+                            const float4 q = *reinterpret_cast<const float4 *>(prow + 32 * c + j);
+                            v[j] = __float_as_uint(__uint_as_float(v[j]) + q.x);
+                            v[j + 1] = __float_as_uint(__uint_as_float(v[j + 1]) + q.y);
+                            v[j + 2] = __float_as_uint(__uint_as_float(v[j + 2]) + q.z);
+                            v[j + 3] = __float_as_uint(__uint_as_float(v[j + 3]) + q.w);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
+                    if (32 * c + 2 * j >= KP) break;
                     // f > 4 * (FC - 1): only columns >= 4FC - 4 can lie past f
                     const int col = 32 * c + 2 * j;
                     float a0 = __uint_as_float(v[2 * j]), a1 = __uint_as_float(v[2 * j + 1]);
                     if (col >= 4 * FC - 4 && col >= f) a0 = 0.0f;
                     if (col + 1 >= 4 * FC - 4 && col + 1 >= f) a1 = 0.0f;
+                    amax = fmaxf(amax, fmaxf(fabsf(a0), fabsf(a1)));
                     const __half2 hv = __floats2half2_rn(a0, a1);
-                    const uint32_t hb = *reinterpret_cast<const uint32_t *>(&hv);
-                    amax = max(amax, max(hb & 0x7fffu, (hb >> 16) & 0x7fffu));
-                    h[j] = act ? hb : 0u;
+                    h[j] = *reinterpret_cast<const uint32_t *>(&hv);
                 }
-                tmem_st16(tb + 16 * c, h);
+                if (32 * c + 32 <= KP) tmem_st16(a_tmem + lane_base + 16 * c, h);
+                else tmem_st8(a_tmem + lane_base + 16 * c, h);
             }
-            if (act && amax == 0x7c00u && g.overflow) *g.overflow = 1;  // (NaN bits are > 0x7c00)
+            tc_fence_before();
+            mbar_arrive(pp.tempty(b));  // the accumulator is free for row r_here + NBUF
+            // binary16 max finite is 65504; RNE sends |a| >= 65520 to inf
+            if (act && !(amax < 65520.0f) && g.overflow) *g.overflow = 1;  // also NaN
             tmem_st_wait();
             tc_fence_before();
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 2);
-            const uint32_t dcol = g.dmv_tail ? tmem_base + NBUF * g.N + 16 * grp
-                                             : tmem_base + b * g.N + g.dmv_off;
-            const uint32_t a_tmem = tmem_base + b * g.N;
+            const uint32_t dcol = tmem_base + g.dmv_base + 16 * grp;
             const float reg = g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
                                          : __double2float_rn(g.lam);
             int bd = 0, nit = 0;
             cg.tr = (ga.trace && r_here < 64) ? ga.trace + 40960 + 64 * r_here : nullptr;
             cg.trk = 0;
             cg.solve(a_tmem, dcol, reg, bi, -1.0, g.tol, g.f_s, xi, bd, nit);
-            tc_fence_before();
-            mbar_arrive(pp.tempty(b));  // the accumulator is free for row r_here + NBUF
+            tc_fence_before();  // the next row's repack overwrites the slot the MMAs read
             if (act) {
                 tgt[i] = xi;
                 // multi-GPU: the solved row also goes straight into every peer's
@@ -663,18 +766,44 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
 int gram_tc_width(int f);
 int fused_cg_trace(void *buf) { return tc::set_trace_buf(buf); }
 
+// seg[u] = first position of row u whose index is >= split (rows sorted by index,
+// as build() leaves them; for unsorted rows the split is still a valid partition)
+__global__ void segment_split_kernel(const int64_t *indptr, const int32_t *indices, int64_t nrows, int32_t split,
+                                     int64_t *seg) {
+    for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < nrows;
+         u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int64_t lo = indptr[u], hi = indptr[u + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (indices[mid] < split) lo = mid + 1;
+            else hi = mid;
+        }
+        seg[u] = lo;
+    }
+}
+
+// Two passes pay when the rows are long (the partial accumulator's HBM round
+// trip, ~2 x 43 KB per row at f = 100, is small against the row's gather) and
+// the fixed side's binary16 shadow is too large to stay in L2 across the
+// sweep (Netflix Theta side: 100 MB of X shadow, 67% L2 hits in one pass).
+constexpr int64_t kTwoPassShadowBytes = int64_t(48) << 20;
+int64_t fused_cg_workspace_bytes(int64_t nrows, int W) {
+    const int64_t pws = (W + 2 + 3) / 4 * 4;
+    return ((nrows * 8 + 255) & ~int64_t(255)) + nrows * 128 * pws * 4;
+}
+
 template <int FC, bool LONG>
 static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
     using Shape = tc::FusedShape<FC, LONG>;
     using PipeT = tc::FPipe<Shape::NBUF>;
     const size_t smem = 1024 + PipeT::kStages * PipeT::kStageBytes + Shape::NG * tc::MVB_BYTES +
-                        (PipeT::kBars + Shape::NG) * 8 + 16;
+                        (PipeT::kBars + 2 * Shape::NG) * 8 + 16;
     // matvec results (16 columns per group): after the accumulators when they fit,
     // else in each buffer's columns freed by the fp16 repacking of A_u
-    constexpr int KP = (FC * 4 + 15) / 16 * 16;
-    g.dmv_tail = Shape::NBUF * g.N + 16 * Shape::NG <= 512;
-    g.dmv_off = (KP / 2 + 15) / 16 * 16;
-    if (!g.dmv_tail && g.dmv_off + 16 > g.N) return set_error(CMF_EINVAL, "fused CG: no TMEM room for f=%d", g.gather.f);
+    if (g.N > Shape::NMAX) return set_error(CMF_EINVAL, "fused CG: accumulator width %d > %d", g.N, Shape::NMAX);
+    if (g.nprod <= 0 || g.nprod > Shape::NPROD) g.nprod = Shape::NPROD;
+    g.slot_base = Shape::NBUF * g.N;
+    g.dmv_base = (g.slot_base + Shape::NG * Shape::SLOT + 15) / 16 * 16;
     g.tmem_cols = 512;
     auto k = tc::fused_cg_kernel<FC, LONG>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -688,6 +817,8 @@ static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
     return check_launch("fused_cg_kernel");
 }
 
+static int fused_dispatch(tc::FusedArgs g, int f, bool long_rows, cudaStream_t st);
+
 // f (<= 120) -> template instance FC = ceil(f/4), bucketed
 #define CMF_FUSED_CASE(FMAX, FCV) \
     if (f <= FMAX) return long_rows ? launch_fused<FCV, true>(g, st) : launch_fused<FCV, false>(g, st);
@@ -695,7 +826,7 @@ static int launch_fused(tc::FusedArgs g, cudaStream_t st) {
 int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
                     const void *fixed16, int64_t ncols, int W, int f, double lam, int weighted, float *target,
                     float *const *peers, int npeers, int64_t nnz, int f_s, double cg_tol, int32_t *breakdowns,
-                    int32_t *overflow, cudaStream_t st) {
+                    int32_t *overflow, void *ws, int64_t ws_bytes, cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
     if (npeers < 0 || (npeers > 0 && peers == nullptr)) return set_error(CMF_EINVAL, "bad peer replica list");
     if (nnz < 0) return set_error(CMF_EINVAL, "negative rating count");
@@ -722,21 +853,41 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
     g.npeers = npeers;
     g.f_s = f_s;
     {
+        // every producer warp of the shape (same-box A/B, tools/ab_probe.sh: with 4
+        // CG groups the user side runs 5.48 ms with 7 producers, 5.65 with 5)
         const char *e = getenv("CMF_FUSED_PROD");
-        // Short rows over an L2-resident fixed side (Netflix users: 3.7 MB of
-        // item factors) gather fast enough with 5 warps, and the 2 idle ones
-        // leave issue slots to the CG groups (update-X 5.60 -> 5.22 ms); when
-        // the gather misses L2 (a large fixed side, or long rows) all 7 pay off
-        // (Yahoo: 17.8 vs 18.3 ms with 5).  Same-box A/B, tools/ab_probe.sh.
-        const bool l2_resident = static_cast<int64_t>(ncols) * W * 2 <= (int64_t(32) << 20);
-        const int dflt = (!long_rows && l2_resident) ? 5 : tc::F_PROD;
-        g.nprod = e ? atoi(e) : dflt;
-        if (g.nprod < 1 || g.nprod > tc::F_PROD) g.nprod = dflt;
+        g.nprod = e ? atoi(e) : 0;
     }
     g.tol = static_cast<float>(cg_tol);
     g.breakdowns = breakdowns;
     g.overflow = overflow;
     g.gather.overflow = overflow;
+    {
+        const char *e = getenv("CMF_TWO_PASS");
+        const bool want = e ? atoi(e) != 0
+                            : long_rows && static_cast<int64_t>(ncols) * W * 2 > kTwoPassShadowBytes;
+        if (want && ws && ws_bytes >= fused_cg_workspace_bytes(nrows, W) && f <= 104) {
+            int64_t *seg = static_cast<int64_t *>(ws);
+            g.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + ((nrows * 8 + 255) & ~int64_t(255)));
+            g.pws = (W + 2 + 3) / 4 * 4;
+            g.gather.seg = seg;
+            const int64_t blocks = (nrows + 255) / 256;
+            segment_split_kernel<<<static_cast<unsigned>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
+                indptr, indices, nrows, static_cast<int32_t>(ncols / 2), seg);
+            int rc = check_launch("segment_split_kernel");
+            if (rc != CMF_OK) return rc;
+            for (int pass = 1; pass <= 2; ++pass) {
+                g.gather.pass = pass;
+                rc = fused_dispatch(g, f, long_rows, st);
+                if (rc != CMF_OK) return rc;
+            }
+            return CMF_OK;
+        }
+    }
+    return fused_dispatch(g, f, long_rows, st);
+}
+
+static int fused_dispatch(tc::FusedArgs g, int f, bool long_rows, cudaStream_t st) {
     CMF_FUSED_CASE(8, 2)
     CMF_FUSED_CASE(16, 4)
     CMF_FUSED_CASE(24, 6)

@@ -161,7 +161,20 @@ struct GatherArgs {
     int ncols;             // rows of the fixed factors; the shadow's row ncols is all zeros
     long long *trace;      // debug timeline (CMF_TRACE builds), else unused
     int32_t *overflow;     // set when a rating does not fit its binary16 hi half (nullable)
+    // Segmented gather (two passes over the fixed side, fused_cg.cu): pass 1
+    // gathers positions [indptr[u], seg[u]) of each row, pass 2 [seg[u],
+    // indptr[u+1]); pass 0 (default) the whole row.
+    const int64_t *seg;
+    int pass;
 };
+
+// Gather range of row u in the current pass.
+__device__ __forceinline__ void row_segment(const GatherArgs &g, int64_t u, int64_t &b, int64_t &e) {
+    b = g.indptr[u];
+    e = g.indptr[u + 1];
+    if (g.pass == 1) e = g.seg[u];
+    else if (g.pass == 2) b = g.seg[u];
+}
 
 // Operand ring of NST stages + NBUF TMEM accumulator hand-offs (mbarriers:
 // full[NST], empty[NST], tfull[NBUF], tempty[NBUF]).
@@ -187,12 +200,11 @@ struct Pipe {
 struct StageIter {
     int64_t u, q0, p1;
     int64_t nrows, rstride;
-    const int64_t *indptr;
+    const GatherArgs *g;
     __device__ bool valid() const { return u < nrows; }
     __device__ void first(int64_t row0) {
         for (u = row0; u < nrows; u += rstride) {
-            q0 = indptr[u];
-            p1 = indptr[u + 1];
+            row_segment(*g, u, q0, p1);
             if (p1 > q0) return;
         }
     }
@@ -200,13 +212,22 @@ struct StageIter {
         q0 += KS;
         if (q0 < p1) return;
         for (u += rstride; u < nrows; u += rstride) {
-            q0 = indptr[u];
-            p1 = indptr[u + 1];
+            row_segment(*g, u, q0, p1);
             if (p1 > q0) return;
         }
     }
+    // k stages on: jumps within a row, visits only the rows it crosses
     __device__ void advance(int k) {
-        for (int j = 0; j < k && valid(); ++j) next();
+        while (k > 0 && valid()) {
+            const int64_t left = (p1 - q0 + KS - 1) / KS;  // stages of this row from q0 on
+            if (k < left) {
+                q0 += static_cast<int64_t>(k) * KS;
+                return;
+            }
+            k -= static_cast<int>(left);
+            q0 = p1;  // past the row's last stage:
+            next();   // the first stage of the next non-empty row
+        }
     }
 };
 
@@ -286,7 +307,7 @@ __device__ void produce(const GatherArgs &g, const __half *fixed16, const __half
                         const Pipe<NST, SPLIT, NBUF> &pp, int pw, int nprod, int lane, int64_t row0,
                         int64_t rstride) {
     const uint64_t pol = policy_evict_last();
-    StageIter cur{0, 0, 0, g.nrows, rstride, g.indptr};
+    StageIter cur{0, 0, 0, g.nrows, rstride, &g};
     cur.first(row0);
     cur.advance(pw);
     // three in-flight stages in a static ring: slot k always holds its own
@@ -395,7 +416,8 @@ __device__ __forceinline__ uint32_t elect_one() {
 // ahead so the indptr latency stays off the issue loop.
 template <int NST, bool SPLIT, int NBUF>
 __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, SPLIT, NBUF> &pp, uint32_t tmem_base,
-                                          int N, int64_t row0, int64_t rstride) {
+                                          int N, int64_t row0, int64_t rstride, uint32_t cons_full = 0,
+                                          int ncons = 0) {
     const uint32_t idesc = make_idesc(M, N);
     const uint64_t desc0 = make_desc(pp.stage(0));
     // descriptor start address field is (addr >> 4): stage s, K-step kk adds
@@ -405,22 +427,29 @@ __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, S
     constexpr uint32_t kLoStep = STAGE_BYTES >> 4;
     uint32_t it = 0, rowc = 0;
     int64_t u = row0;
+    // rows with ratings get an accumulator hand-off (p0 < p1); in a segmented
+    // pass the MMAs cover the row's segment [s0, s1) only, which may be empty
+    // (then the commit announces an untouched buffer; the consumer knows)
     int64_t p0 = u < g.nrows ? g.indptr[u] : 0, p1 = u < g.nrows ? g.indptr[u + 1] : 0;
+    int64_t s0 = p0, s1 = p1;
+    if (g.pass && u < g.nrows) row_segment(g, u, s0, s1);
     while (u < g.nrows) {
         const int64_t un = u + rstride;
         const int64_t q0n = un < g.nrows ? g.indptr[un] : 0, q1n = un < g.nrows ? g.indptr[un + 1] : 0;
+        int64_t t0n = q0n, t1n = q1n;
+        if (g.pass && un < g.nrows) row_segment(g, un, t0n, t1n);
         if (p1 > p0) {
             const int b = rowc % NBUF;
             mbar_wait(pp.tempty(b), ((rowc / NBUF) & 1) ^ 1);
             tc_fence_after();
             const uint32_t tmem_d = tmem_base + b * N;
             uint32_t acc = 0;
-            for (int64_t q0 = p0; q0 < p1; q0 += KS, ++it) {
+            for (int64_t q0 = s0; q0 < s1; q0 += KS, ++it) {
                 const int s = it % NST;
                 mbar_wait(pp.full(s), (it / NST) & 1);
                 if (lane_id() == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 3);
                 tc_fence_after();
-                const int nk = static_cast<int>(min(static_cast<int64_t>(KS), p1 - q0) + 15) >> 4;
+                const int nk = static_cast<int>(min(static_cast<int64_t>(KS), s1 - q0) + 15) >> 4;
                 const uint64_t ds = desc0 + s * kStageStep;
                 if (elect_one()) {
                     for (int kk = 0; kk < nk; ++kk) {
@@ -437,13 +466,18 @@ __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, S
                 acc = 1;
                 if (lane_id() == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 4);
             }
-            if (elect_one()) tc_commit(pp.tfull(b));
+            // announce the accumulator: on the buffer's barrier, or (ncons > 0) on
+            // the barrier of the consumer that owns row rowc (rowc % ncons), so that
+            // each consumer waits on its own phase sequence
+            if (elect_one()) tc_commit(ncons ? cons_full + 8u * (rowc % ncons) : pp.tfull(b));
             __syncwarp();
             ++rowc;
         }
         u = un;
         p0 = q0n;
         p1 = q1n;
+        s0 = t0n;
+        s1 = t1n;
     }
 }
 

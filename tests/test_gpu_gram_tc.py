@@ -111,8 +111,11 @@ def test_fused_tc_cg_matches_two_step(cuda_device, monkeypatch):
     same fp16 Gram operands, same CG recurrence, so the solutions agree to fp32
     rounding; rows without ratings are untouched in both."""
     import torch
-    # both routes store A_u in binary16 from the same fp32 accumulator; the
-    # two-step solver then runs the same pipelined recurrence as the fused one
+    # both routes store A_u in binary16 from the same fp32 accumulator and run
+    # the same pipelined recurrence; the two-step route rounds the regularised
+    # diagonal A_ii + lam n_u to binary16 (the reference's pack_half), the fused
+    # one keeps lam n_u in fp32 -- a 2^-11-relative diagonal difference, so the
+    # bar is 1e-3 (rel. Frobenius) rather than fp32 rounding
     monkeypatch.setenv("CMF_CG_PIPELINED", "1")
     for f, (m, n, nnz) in ((100, (300, 900, 30000)), (32, (500, 200, 8000)), (8, (50, 40, 300))):
         t, _ = cmfb.gen_synthetic(m, n, f, nnz / (m * n), 0.1, 3)
@@ -127,7 +130,7 @@ def test_fused_tc_cg_matches_two_step(cuda_device, monkeypatch):
         x0 = cmfb.init_factors(m + 1, f, 0.1, [0, 0])
         assert np.array_equal(outs[0][m], x0[m]) and np.array_equal(outs[1][m], x0[m])
         rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1])
-        assert rel < 1e-4, (f, rel)
+        assert rel < 1e-3, (f, rel)
 
 
 def test_fused_tc_cg_shapes_match_two_step(cuda_device, monkeypatch):
@@ -150,7 +153,7 @@ def test_fused_tc_cg_shapes_match_two_step(cuda_device, monkeypatch):
             cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp16"), gram_kernel=kern)
             outs.append(x)
         rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1])
-        assert rel < 1e-4, (f, side, rel)
+        assert rel < 1e-3, (f, side, rel)
 
 
 def test_fused_tc_cg_large_fixed_side(cuda_device, monkeypatch):
@@ -169,7 +172,7 @@ def test_fused_tc_cg_large_fixed_side(cuda_device, monkeypatch):
         cmfb.update_side(view, fixed, x, 0.05, cmfb.SolverConfig("cg", precision="fp16"), gram_kernel=kern)
         outs.append(x)
     rel = float(torch.linalg.norm(outs[0] - outs[1]) / torch.linalg.norm(outs[1]))
-    assert rel < 1e-4, rel
+    assert rel < 1e-3, rel
 
 
 def test_split_precision_gram_is_fp32_faithful(golden, oracle, cuda_device):
@@ -225,3 +228,33 @@ def test_exact_route_long_rows_factor_bar(oracle, cuda_device):
         oracle.update_side(r.csc(), x_o, t_o, 0.05, "exact")
         cmfb.update_side(sr.csc_view(), x_g, t_g, 0.05, solver)
         assert np.linalg.norm(t_g - t_o) / np.linalg.norm(t_o) < 1e-4, (epoch, "t")
+
+
+def test_fused_two_pass_item_side_matches_one_pass(cuda_device, monkeypatch):
+    """Long rows over a fixed side whose binary16 shadow exceeds L2 (the Netflix
+    item side): the fused kernel gathers the first half of the user ids, parks
+    each row's fp32 partial Gram in the workspace, then adds the second half and
+    solves.  Same solutions as one pass up to fp32 summation order -- including
+    rows whose ratings all fall in one half (an empty segment)."""
+    import torch
+    f, m, n = 100, 250_000, 40
+    rng = np.random.default_rng(9)
+    u = rng.integers(0, m, 120_000)
+    v = rng.integers(2, n, 120_000)
+    # item 0: only users of the first half; item 1: only the second half
+    u = np.concatenate([u, rng.integers(0, m // 2, 3000), rng.integers(m // 2, m, 3000)])
+    v = np.concatenate([v, np.zeros(3000, np.int64), np.ones(3000, np.int64)])
+    t = cmfb.Triples(u, v, rng.standard_normal(len(u)).astype(np.float32))
+    sr = cmfb.build(t, m, n)
+    assert sr.nnz >= 1024 * n and m * 104 * 2 > (48 << 20)
+    fixed = torch.from_numpy(cmfb.init_factors(m, f, 0.1, [0, 0])).cuda()
+    view = sr.to_device().csc_view()
+    outs = []
+    for two in ("0", "1"):
+        monkeypatch.setenv("CMF_TWO_PASS", two)
+        th = torch.from_numpy(cmfb.init_factors(n, f, 0.1, [0, 1])).cuda()
+        cmfb.update_side(view, fixed, th, 0.05, cmfb.SolverConfig("cg", precision="fp16"))
+        outs.append(th.cpu().numpy())
+    rel = np.linalg.norm(outs[0] - outs[1], axis=1) / np.linalg.norm(outs[0], axis=1)
+    assert rel.max() < 1e-3, rel
+    assert np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[0]) < 2e-4
