@@ -15,6 +15,9 @@ KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Cache Throughput
         "Achieved Occupancy", "Dynamic Shared Memory Per Block", "Grid Size", "Block Size"]
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum",
        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+       "sm__inst_issued.avg.pct_of_peak_sustained_active",
+       "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+       "lts__t_sector_hit_rate.pct",
        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
        "gpu__time_duration.sum"]
 
@@ -67,8 +70,9 @@ def report(path):
                 print(f"| {key} | {d[key][0]} {d[key][1]} |")
         if k < len(vals):
             for key in RAW:
-                if key in hdr:
-                    i = hdr.index(key)
+                # raw-page columns may carry a section prefix ("TPC.TriageCompute.<metric>")
+                i = next((j for j, h in enumerate(hdr) if h == key or h.endswith("." + key)), None)
+                if i is not None:
                     print(f"| {key} | {vals[k][i]} {units[i]} |")
         print()
 
