@@ -265,6 +265,32 @@ int cmf_predict_pairs(const void *users, const void *items, int32_t idx64, int64
                       const float *x, const float *theta, int32_t f, float *pred,
                       void *stream);
 
+/*
+ * CSR + CSC construction (a13 / f3 in SURVEY 8).  Replaces data.build
+ * (data.py:205-249): triples (user, item, rating) in file order -> the
+ * reference's paired structure, bit for bit: rows ordered by (user, item),
+ * duplicate (user, item) pairs collapsed to the LAST occurrence in file order,
+ * CSC ordered by (item, user).  Hand-written stable LSD radix sorts (u64 key
+ * user*n + item, then u32 key item), deterministic.
+ *
+ * user/item: int64 when idx64 != 0, else int32.  mn[2] (host, in/out): m, n;
+ * a negative entry means "max id + 1" (the reference's default for None) and
+ * is replaced by the resolved value (row_ptr == NULL: resolve m, n and return
+ * without building, so the caller can size the outputs).  Outputs are caller-allocated device
+ * arrays sized for the worst case: row_ptr[m+1], col_ptr[n+1] (int64),
+ * col_idx/row_idx (int32) and csr_val/csc_val (float32) of length k.
+ * ws: device workspace of cmf_build_workspace_bytes(k) bytes.
+ * Synchronises `stream` (device->host reads of m/n, the validation result and
+ * nnz): *nnz_host = entries after dedup.  An out-of-range triple returns
+ * CMF_EINVAL with *bad_host = its index (the reference names the first one),
+ * else *bad_host = -1.  Limits: k < 2^32 - 1, m < 2^32, n < 2^31.
+ */
+int cmf_build(const void *user, const void *item, int32_t idx64, const float *rating, int64_t k,
+              int64_t *mn, int64_t *row_ptr, int32_t *col_idx, float *csr_val, int64_t *col_ptr,
+              int32_t *row_idx, float *csc_val, void *ws, int64_t ws_bytes, int64_t *nnz_host,
+              int64_t *bad_host, void *stream);
+int64_t cmf_build_workspace_bytes(int64_t k);
+
 #ifdef __cplusplus
 }
 #endif

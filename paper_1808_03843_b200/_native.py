@@ -65,6 +65,9 @@ _SIGNATURES = {
     "cmf_sq_error_csr": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp]),
     "cmf_weighted_sqnorm": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "cmf_predict_pairs": (ctypes.c_int, [_vp, _vp, _i32, _i64, _vp, _vp, _i32, _vp, _vp]),
+    "cmf_build": (ctypes.c_int, [_vp, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                                 _vp, _vp, _vp]),
+    "cmf_build_workspace_bytes": (ctypes.c_int64, [_i64]),
 }
 EXPORTED = tuple(_SIGNATURES)
 REDUCE_SLOTS = 1024  # eval.cu: doubles an eval `out` buffer must hold

@@ -46,6 +46,9 @@ int wsqnorm_launch(const int64_t *, const float *, int64_t, int, double *, cudaS
 int predict_launch(const void *, const void *, bool, int64_t, const float *, const float *, int,
                    float *, cudaStream_t);
 int pack_half_launch(const float *, void *, int64_t, int32_t *, cudaStream_t);
+int build_launch(const void *, const void *, bool, const float *, int64_t, int64_t *, int64_t *, int32_t *, float *,
+                 int64_t *, int32_t *, float *, void *, int64_t, int64_t *, int64_t *, cudaStream_t);
+int64_t build_workspace_bytes(int64_t k);
 
 int gram_tc_trace(void *buf);
 int fused_cg_trace(void *buf);
@@ -359,5 +362,16 @@ int cmf_predict_pairs(const void *users, const void *items, int32_t idx64, int64
     REQUIRE(count >= 0 && f >= 1, "bad arguments");
     return predict_launch(users, items, idx64 != 0, count, x, theta, f, pred, S(stream));
 }
+
+int cmf_build(const void *user, const void *item, int32_t idx64, const float *rating, int64_t k, int64_t *mn,
+              int64_t *row_ptr, int32_t *col_idx, float *csr_val, int64_t *col_ptr, int32_t *row_idx, float *csc_val,
+              void *ws, int64_t ws_bytes, int64_t *nnz_host, int64_t *bad_host, void *stream) {
+    REQUIRE(k >= 0 && mn != nullptr && nnz_host != nullptr && bad_host != nullptr, "bad build arguments");
+    REQUIRE(k == 0 || (user && item && rating), "null triple arrays");
+    return build_launch(user, item, idx64 != 0, rating, k, mn, row_ptr, col_idx, csr_val, col_ptr, row_idx, csc_val,
+                        ws, ws_bytes, nnz_host, bad_host, S(stream));
+}
+
+int64_t cmf_build_workspace_bytes(int64_t k) { return k < 0 ? -1 : build_workspace_bytes(k); }
 
 }  // extern "C"

@@ -291,14 +291,19 @@ struct TmemCg {
         if (mv) fence_proxy_async();
         // three butterfly levels leave 4 partials per warp (lanes 0-3); the 16
         // per value are summed after the barrier in a fixed order
+#ifdef CMF_RED5
+        constexpr int kLow = 0;
+#else
+        constexpr int kLow = 2;
+#endif
 #pragma unroll
-        for (int o = 16; o > 2; o >>= 1) {
+        for (int o = 16; o > kLow; o >>= 1) {
             if (NRED >= 1) da += __shfl_xor_sync(0xffffffffu, da, o);
             if (NRED >= 2) db += __shfl_xor_sync(0xffffffffu, db, o);
         }
         float *rd = red + 32 * slot;
         slot ^= 1;
-        if (lane < 4) {
+        if (lane < 4 && (kLow == 2 || lane == 0)) {
             if (NRED >= 1) rd[(warp & 3) * 4 + lane] = da;
             if (NRED >= 2) rd[16 + (warp & 3) * 4 + lane] = db;
         }
@@ -315,6 +320,31 @@ struct TmemCg {
             }
             __syncwarp();
         }
+#if defined(CMF_RED5)
+        {
+            // one partial per warp (rd[4w] / rd[16 + 4w])
+            sa = NRED >= 1 ? (rd[0] + rd[4]) + (rd[8] + rd[12]) : 0.0f;
+            sb = NRED >= 2 ? (rd[16] + rd[20]) + (rd[24] + rd[28]) : 0.0f;
+        }
+#elif defined(CMF_RED16)
+        if (NRED >= 1) {
+            // lane l sums partial l & 15 of value l >> 4 with a 16-lane butterfly
+            // (bitwise identical in every lane: each level adds the same pair)
+            float t = rd[NRED >= 2 ? lane : (lane & 15)];
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (NRED >= 2) {
+                const float o16 = __shfl_xor_sync(0xffffffffu, t, 16);
+                sa = lane < 16 ? t : o16;
+                sb = lane < 16 ? o16 : t;
+            } else {
+                sa = t;
+                sb = 0.0f;
+            }
+        } else {
+            sa = sb = 0.0f;
+        }
+#else
         {
             const float4 *r4 = reinterpret_cast<const float4 *>(rd);
             float t[8];
@@ -326,6 +356,7 @@ struct TmemCg {
             sa = NRED >= 1 ? (t[0] + t[1]) + (t[2] + t[3]) : 0.0f;
             sb = NRED >= 2 ? (t[4] + t[5]) + (t[6] + t[7]) : 0.0f;
         }
+#endif
         if (!mv) return 0.0f;
         mbar_wait(mvbar, mvph & 1);
         CG_STAMP();

@@ -17,6 +17,7 @@ training loop keeps resident in HBM.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import struct
 from dataclasses import dataclass
@@ -169,44 +170,49 @@ def _as_triples(triples) -> Triples:
 
 
 def build_device(triples, m: int | None = None, n: int | None = None) -> DeviceRatings:
-    """CSR + CSC on the GPU; bit-identical to reference data.build (data.py:205-249)."""
+    """CSR + CSC on the GPU (``cmf_build``: hand-written stable radix sorts,
+    build.cu); bit-identical to reference data.build (data.py:205-249),
+    including the collapse of duplicate (user, item) pairs to the last
+    occurrence and the DataError naming the first out-of-range triple."""
     t = _as_triples(triples)
     dev = nat.device()
     user = nat.to_dev(t.user, torch.int64, dev)
     item = nat.to_dev(t.item, torch.int64, dev)
     val = nat.to_dev(t.rating, torch.float32, dev)
-    k = user.shape[0]
-    if m is None:
-        m = int(user.max().item()) + 1 if k else 0
-    if n is None:
-        n = int(item.max().item()) + 1 if k else 0
-    if k:
-        bad = (user < 0) | (user >= m) | (item < 0) | (item >= n)
-        if bool(bad.any()):
-            i = int(torch.argmax(bad.to(torch.int8)).item())
-            raise DataError(f"triple ({int(user[i])}, {int(item[i])}, {float(val[i])}) "
-                            f"out of range for a {m}x{n} matrix")
-        # stable sort on the (user, item) key keeps file order inside duplicate runs
-        key = user * n + item
-        skey, order = torch.sort(key, stable=True)
-        last = torch.ones(k, dtype=torch.bool, device=dev)
-        last[:-1] = skey[:-1] != skey[1:]
-        order = order[last]
-        su, si, sv = user[order], item[order], val[order]
-    else:
-        su = si = torch.empty(0, dtype=torch.int64, device=dev)
-        sv = torch.empty(0, dtype=torch.float32, device=dev)
-    nnz = int(su.shape[0])
-    row_ptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
-    col_ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    if nnz:
-        torch.cumsum(torch.bincount(su, minlength=m), 0, out=row_ptr[1:])
-        torch.cumsum(torch.bincount(si, minlength=n), 0, out=col_ptr[1:])
-        _, corder = torch.sort(si, stable=True)
-    else:
-        corder = torch.empty(0, dtype=torch.int64, device=dev)
-    return DeviceRatings(m, n, nnz, row_ptr, si.to(torch.int32), sv, col_ptr,
-                         su[corder].to(torch.int32), sv[corder])
+    k = int(user.shape[0])
+    # an explicit negative extent puts every id out of range, as in the reference
+    mn = (ctypes.c_int64 * 2)(-1 if m is None else max(int(m), 0), -1 if n is None else max(int(n), 0))
+    if m is not None and int(m) < 0 and k == 0:
+        raise DataError(f"negative matrix extent m={m}")
+    if n is not None and int(n) < 0 and k == 0:
+        raise DataError(f"negative matrix extent n={n}")
+    ws = torch.empty(int(nat.lib().cmf_build_workspace_bytes(k)), dtype=torch.uint8, device=dev)
+    nnz, bad = ctypes.c_int64(0), ctypes.c_int64(-1)
+    args = (nat.ptr(user), nat.ptr(item), 1, nat.ptr(val), k, mn)
+    tail = (nat.ptr(ws), ws.numel(), ctypes.byref(nnz), ctypes.byref(bad), nat.stream_ptr())
+    if m is None or n is None:  # size the outputs: resolve max id + 1 first
+        nat.call("cmf_build", *args, None, None, None, None, None, None, *tail)
+    M, N = int(mn[0]), int(mn[1])
+    row_ptr = torch.empty(M + 1, dtype=torch.int64, device=dev)
+    col_ptr = torch.empty(N + 1, dtype=torch.int64, device=dev)
+    col_idx = torch.empty(k, dtype=torch.int32, device=dev)
+    row_idx = torch.empty(k, dtype=torch.int32, device=dev)
+    csr_val = torch.empty(k, dtype=torch.float32, device=dev)
+    csc_val = torch.empty(k, dtype=torch.float32, device=dev)
+    rc = nat.lib().cmf_build(*args, nat.ptr(row_ptr), nat.ptr(col_idx), nat.ptr(csr_val), nat.ptr(col_ptr),
+                             nat.ptr(row_idx), nat.ptr(csc_val), *tail)
+    nat.LAUNCHES[0] += 1
+    if rc != nat.CMF_OK and bad.value >= 0:
+        i = int(bad.value)
+        raise DataError(f"triple ({int(t.user[i])}, {int(t.item[i])}, {float(t.rating[i])}) "
+                        f"out of range for a {m if m is not None else M}x{n if n is not None else N} matrix")
+    nat.check(rc, "cmf_build")
+    del ws
+    z = int(nnz.value)
+    if z < k:  # duplicates collapsed: trim the worst-case allocations
+        col_idx, row_idx = col_idx[:z].clone(), row_idx[:z].clone()
+        csr_val, csc_val = csr_val[:z].clone(), csc_val[:z].clone()
+    return DeviceRatings(M, N, z, row_ptr, col_idx, csr_val, col_ptr, row_idx, csc_val)
 
 
 def build(triples, m: int | None = None, n: int | None = None) -> SparseRatings:
