@@ -593,17 +593,27 @@ def next_rows(cmfb, train, test, x0, th0, m, n):
     x, th = x0.clone(), th0.clone()
     out["test_rmse_ms"] = timed(lambda: cmfb.rmse(x, th, test), 3)
     out["objective_ms"] = timed(lambda: cmfb.objective(x, th, train, 0.05), 3)
-    solver = cmfb.SolverConfig("cg")
     csr = cmfb.RowView(train.row_ptr, train.col_idx, train.csr_val.abs(), m, n)
     csc = cmfb.RowView(train.col_ptr, train.row_idx, train.csc_val.abs(), n, m)
 
-    def implicit_iteration():
-        implicit_update_side(csr, th, precompute_gram(th), x, 40.0, 0.05, solver, gram_kernel="fma")
-        implicit_update_side(csc, x, precompute_gram(x), th, 40.0, 0.05, solver, gram_kernel="fma")
+    def implicit_iteration(solver, kernel, alpha=40.0):
+        # from the bench's init factors every time (|r| as the implicit counts)
+        xi, ti = x0.clone(), th0.clone()
+        implicit_update_side(csr, ti, precompute_gram(ti), xi, alpha, 0.05, solver, gram_kernel=kernel)
+        implicit_update_side(csc, xi, precompute_gram(xi), ti, alpha, 0.05, solver, gram_kernel=kernel)
 
-    out["implicit_iteration_ms"] = timed(implicit_iteration, 2)
-    out["note"] = ("device time on the bench data; implicit = weighted FMA Gram + CG fp32, "
-                   "f_s = 6 (the tensor-core route has no per-rating operand weights yet)")
+    s16 = cmfb.SolverConfig("cg", precision="fp16")
+    for alpha in (40.0, 1.0):  # binary16 A overflows (NumericalError, as in the reference) for large alpha
+        try:
+            out["implicit_iteration_ms"] = timed(lambda: implicit_iteration(s16, None, alpha), 3)
+            out["implicit_alpha"] = alpha
+            break
+        except cmfb.NumericalError:
+            out["implicit_overflow_at_alpha"] = alpha
+    out["implicit_iteration_fp32_ms"] = timed(lambda: implicit_iteration(cmfb.SolverConfig("cg"), "fma"), 1)
+    out["note"] = ("device time on the bench data (f_s = 6, |r| as counts); implicit = the fused "
+                   "tensor-core kernel with per-rating operand weights (cg16: binary16 A, fp32 vectors) + "
+                   "the F^T F base; implicit_fp32 = weighted FMA Gram + fp32 CG (precision='fp32')")
     return out
 
 

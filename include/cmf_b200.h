@@ -160,7 +160,30 @@ int cmf_fused_cg_update_ws(const int64_t *indptr, const int32_t *indices, const 
                            float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
                            int32_t *breakdowns, int32_t *overflow_flag, void *workspace,
                            int64_t workspace_bytes, void *stream);
+/*
+ * Implicit-feedback half-update on the fused CG route (f1 in SURVEY 8):
+ * replaces implicit.implicit_update_side (implicit.py:63-84) with
+ * precision="fp16" for every row with observations:
+ *   A_u = gram_full + sum_k alpha r_k theta_k theta_k^T + lam I   (plain lambda)
+ *   b_u = sum_k (1 + alpha r_k) theta_k
+ * gram_full: F^T F of the fixed factors as a full row-major float32 matrix,
+ * f rows of stride cmf_fused_base_ld(f) floats (implicit.precompute_gram,
+ * unpacked; the stride is the kernel instance's compile-time row width).  The Gram runs on tcgen05 with
+ * the gathered binary16 rows against a weighted copy (alpha r_k theta_k,
+ * binary16) written by the producer warps; the CG, the overflow flag and the
+ * workspace are as cmf_fused_cg_update_ws.  Rows with n_u == 0 are NOT touched
+ * (their system is gram_full + lam I with b = 0, one shared matrix: the caller
+ * solves them with cmf_batch_cg and a_stride = 0).  values must be >= 0.
+ */
+int cmf_fused_cg_update_implicit(const int64_t *indptr, const int32_t *indices, const float *values,
+                                 int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
+                                 int32_t f, double alpha, double lam, const float *gram_full, float *target,
+                                 float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
+                                 int32_t *breakdowns, int32_t *overflow_flag, void *workspace,
+                                 int64_t workspace_bytes, void *stream);
 int64_t cmf_fused_cg_workspace_bytes(int64_t nrows, int32_t f);
+/* Row stride (floats) of cmf_fused_cg_update_implicit's gram_full; -1 if f > 120. */
+int32_t cmf_fused_base_ld(int32_t f);
 /* CUDA IPC for the peer replicas: export a device pointer (any address inside
  * an allocation) as a 64-byte handle + offset; open it in another process
  * (peer access enabled lazily over NVLink); close with the same offset. */
@@ -200,6 +223,8 @@ int cmf_spmm_bias(const int64_t *indptr, const int32_t *indices, const float *b_
  *   not written (als.py:69-72 compaction, done in place).
  *   x0 and x_out may alias (in-place warm start).  iters/broke nullable.
  *   *breakdowns (device int, nullable) accumulates the breakdown count.
+ *   a_stride == 0: every system shares the one matrix at `a` (the implicit
+ *   engine's rows without observations: F^T F + lam I, b = 0).
  */
 int cmf_batch_cg(const void *a, int32_t a_precision, int64_t a_stride, const float *b,
                  const float *x0, const double *eps, double cg_tol, const int64_t *nu,

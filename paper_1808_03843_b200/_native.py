@@ -51,6 +51,9 @@ _SIGNATURES = {
     "cmf_fused_cg_update_ws": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32,
                                               _vp, _vp, _i32, _i32, _f64, _vp, _vp, _vp, _i64, _vp]),
     "cmf_fused_cg_workspace_bytes": (ctypes.c_int64, [_i64, _i32]),
+    "cmf_fused_base_ld": (ctypes.c_int32, [_i32]),
+    "cmf_fused_cg_update_implicit": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _f64,
+                                                    _vp, _vp, _vp, _i32, _i32, _f64, _vp, _vp, _vp, _i64, _vp]),
     "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp]),
     "cmf_spmm_bias": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),
     "cmf_batch_cg": (ctypes.c_int, [_vp, _i32, _i64, _vp, _vp, _vp, _f64, _vp, _i64, _i32, _i32,
@@ -122,7 +125,7 @@ def check(rc: int, what: str = ""):
 
 # Kernel-launching entry points called since the counter was last reset (the
 # benchmark's "gpu_launches" claim counts launches of OUR kernels).
-_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_fused_cg_update_ws": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
+_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_fused_cg_update_ws": 1, "cmf_fused_cg_update_implicit": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
                 "cmf_batch_cholesky": 1, "cmf_pack_half": 1, "cmf_sq_error": 2,
                 "cmf_sq_error_csr": 2, "cmf_weighted_sqnorm": 2, "cmf_predict_pairs": 1}
 LAUNCHES = [0]

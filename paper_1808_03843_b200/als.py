@@ -186,13 +186,17 @@ class HalfUpdatePlan:
 
     def launch(self, indptr, indices, values, fx, tg, lam, weighted_reg, kernel, record=None,
                row0: int = 0, nrows: int | None = None, reuse_shadow: bool = False,
-               nnz: int | None = None, peers=None):
+               nnz: int | None = None, peers=None, implicit=None):
         """Gram(+bias) -> solve for rows [row0, row0+nrows) of the view, block by
         block, solutions written into tg (rows indexed like the view).  ``nnz``:
         ratings in those rows (default: all of the view's), which picks the
         fused kernel's CTA shape.  ``peers``: device int64 tensor of replica
         pointers (offset like ``tg``) that the fused kernel also stores each
-        solved row into (multi-GPU, distributed.ShardedALS)."""
+        solved row into (multi-GPU, distributed.ShardedALS).  ``implicit``:
+        (alpha, gram_full) -- the implicit-feedback system (implicit.py:63-84)
+        on the fused route: per-rating operand weights alpha*r, confidences
+        1 + alpha*r, base F^T F (device fp32, f rows of stride roundup4(f)),
+        plain lambda; rows without ratings are left to the caller."""
         f, solver = self.f, self.solver
         nrows = self.nrows if nrows is None else nrows
         st = nat.stream_ptr()
@@ -230,8 +234,14 @@ class HalfUpdatePlan:
             if nnz >= 1024 * max(nrows, 1) and fx.shape[0] * self.w16 * 2 > (48 << 20):
                 wsb = int(nat.lib().cmf_fused_cg_workspace_bytes(nrows, f))
                 ws = _WS.get(self.dev, wsb, key="fused2p")
-            nat.call("cmf_fused_cg_update_ws", *common, nat.ptr(peers) if npeers else None, npeers,
-                     tail[0], tail[1], tail[2], tail[3], nat.ptr(ws), wsb, tail[4])
+            if implicit is not None:
+                alpha, gram_full = implicit
+                nat.call("cmf_fused_cg_update_implicit", *common[:9], float(alpha), float(lam),
+                         nat.ptr(gram_full), common[11], nat.ptr(peers) if npeers else None, npeers,
+                         tail[0], tail[1], tail[2], tail[3], nat.ptr(ws), wsb, tail[4])
+            else:
+                nat.call("cmf_fused_cg_update_ws", *common, nat.ptr(peers) if npeers else None, npeers,
+                         tail[0], tail[1], tail[2], tail[3], nat.ptr(ws), wsb, tail[4])
             if record is not None:
                 e1.record()
                 record.setdefault("fused_tc_cg", []).append((e0, e1))

@@ -28,7 +28,7 @@ int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, in
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
                     int, float *, float *const *, int, int64_t, int, double, int32_t *, int32_t *, void *, int64_t,
-                    cudaStream_t);
+                    const float *, float, bool, cudaStream_t);
 int64_t fused_cg_workspace_bytes(int64_t nrows, int W);
 int factors_to_half_launch(const float *, int64_t, int, void *, int, int32_t *, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
@@ -49,6 +49,7 @@ int pack_half_launch(const float *, void *, int64_t, int32_t *, cudaStream_t);
 int build_launch(const void *, const void *, bool, const float *, int64_t, int64_t *, int64_t *, int32_t *, float *,
                  int64_t *, int32_t *, float *, void *, int64_t, int64_t *, int64_t *, cudaStream_t);
 int64_t build_workspace_bytes(int64_t k);
+int fused_base_ld(int f);
 
 int gram_tc_trace(void *buf);
 int fused_cg_trace(void *buf);
@@ -206,7 +207,8 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
     REQUIRE(indptr && fixed16 && target, "null argument");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, nullptr,
-                           0, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, S(stream));
+                           0, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, nullptr, 0.0f, false,
+                           S(stream));
 }
 
 int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, const float *values,
@@ -223,7 +225,8 @@ int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, con
     REQUIRE(npeers == 0 || peer_targets, "null peer list");
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
-                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, S(stream));
+                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, nullptr, 0.0f,
+                           false, S(stream));
 }
 
 int cmf_fused_cg_update_ws(const int64_t *indptr, const int32_t *indices, const float *values,
@@ -244,8 +247,32 @@ int cmf_fused_cg_update_ws(const int64_t *indptr, const int32_t *indices, const 
     REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 255) == 0, "workspace must be 256-byte aligned");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
                            peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, workspace,
-                           workspace_bytes, S(stream));
+                           workspace_bytes, nullptr, 0.0f, false, S(stream));
 }
+
+int cmf_fused_cg_update_implicit(const int64_t *indptr, const int32_t *indices, const float *values,
+                                 int64_t nrows, int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16,
+                                 int32_t f, double alpha, double lam, const float *gram_full, float *target,
+                                 float *const *peer_targets, int32_t npeers, int32_t f_s, double cg_tol,
+                                 int32_t *breakdowns, int32_t *overflow_flag, void *workspace,
+                                 int64_t workspace_bytes, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(f_s >= 1, "cg_iters must be >= 1");
+    REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
+    REQUIRE(alpha > 0.0, "alpha must be > 0");
+    REQUIRE(npeers >= 0 && npeers <= 64, "npeers must be in [0, 64]");
+    REQUIRE(workspace_bytes >= 0, "negative workspace size");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && fixed16 && target && values, "null argument");
+    REQUIRE(npeers == 0 || peer_targets, "null peer list");
+    REQUIRE(ncols >= 1, "ncols must be >= 1");
+    REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 255) == 0, "workspace must be 256-byte aligned");
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, 0, target, peer_targets,
+                           npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, workspace, workspace_bytes, gram_full,
+                           static_cast<float>(alpha), true, S(stream));
+}
+
+int32_t cmf_fused_base_ld(int32_t f) { return f < 1 ? -1 : fused_base_ld(f); }
 
 int64_t cmf_fused_cg_workspace_bytes(int64_t nrows, int32_t f) {
     if (nrows < 0 || f < 1) return 0;
@@ -270,7 +297,8 @@ int cmf_batch_cg(const void *a, int32_t a_precision, int64_t a_stride, const flo
     REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
     REQUIRE(a_precision == CMF_PREC_FP32 || a_precision == CMF_PREC_FP16, "unknown precision");
     REQUIRE(accum == CMF_CG_FP32 || accum == CMF_CG_FP64, "unknown accumulation mode");
-    REQUIRE(a_stride >= f * (int64_t)(f + 1) / 2, "a_stride smaller than f*(f+1)/2");
+    REQUIRE(a_stride == 0 || a_stride >= f * (int64_t)(f + 1) / 2,
+            "a_stride must be 0 (one shared matrix) or >= f*(f+1)/2");
     if (nsys == 0) return CMF_OK;
     REQUIRE(a && b && x0 && x_out, "null argument");
     return cg_launch(a, a_precision == CMF_PREC_FP16, a_stride, b, x0, eps, cg_tol, nu, nsys, f, f_s,

@@ -407,6 +407,150 @@ __device__ void produce(const GatherArgs &g, const __half *fixed16, const __half
     }
 }
 
+// Implicit-feedback producers (Pipe<NST, true, NBUF> stages = [gathered rows |
+// weighted copy]), two decoupled roles so that no warp waits on its own copies:
+//   gather_weighted (warp pw of ngath): stage it = pw, pw + ngath, ...: wait for
+//     the slot, gather the 64 factor rows with cp.async into the first half
+//     exactly as produce() does, and let the copies arrive on landed[s] (32
+//     noinc arrivals, one per lane);
+//   scale_weighted (warp pw of nscal): stage it = pw, pw + nscal, ...: load the
+//     stage's ratings, wait for landed[s], write the weighted copy
+//     w_k theta_k (w = alpha r_k, binary16 HMUL2) and the confidence rows
+//     c_k = 1 + alpha r_k (fp16 hi/lo, operand rows W, W+1) into the second
+//     half, fence, and arrive on full[s] (count 1).
+// The MMA then reads gathered x weighted: D = sum_k theta_k (alpha r_k theta_k)^T
+// and D[:, W] + D[:, W+1] = sum_k c_k theta_k (implicit.py:63-84).
+template <int NST, int NBUF>
+__device__ void gather_weighted(const GatherArgs &g, const __half *fixed16, int W, const Pipe<NST, true, NBUF> &pp,
+                                uint32_t landed, int pw, int ngath, int lane, int64_t row0, int64_t rstride) {
+    const uint64_t pol = policy_evict_last();
+    StageIter cur{0, 0, 0, g.nrows, rstride, &g};
+    cur.first(row0);
+    cur.advance(pw);
+    const int c = lane & 15, hrow = lane >> 4;
+    const bool live = c < (W >> 3);
+    const uint32_t W2 = static_cast<uint32_t>(W) * 2;
+    const uint64_t src_hi = reinterpret_cast<uint64_t>(fixed16) + c * 16;
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int t4 = 0; t4 < 4; ++t4) dst_off[t4] = operand_addr(0, 2 * t4 + hrow, c);
+    uint32_t it = pw;
+    StagePairs qn;  // the next stage's pairs, loaded one stage ahead
+    qn.load(g, cur, lane);
+    while (cur.valid()) {
+        StagePairs q = qn;
+        const int nrem16 = static_cast<int>(min(static_cast<int64_t>(KS), cur.p1 - cur.q0) + 15) & ~15;
+        cur.advance(ngath);
+        qn.load(g, cur, lane);
+        const int s = it % NST;
+        q.clamp_ids(g.ncols);
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 0);
+        mbar_wait_backoff(pp.empty(s), ((it / NST) & 1) ^ 1);
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 1);
+        const uint32_t stg = pp.stage(s);
+#pragma unroll
+        for (int t = 0; t < KS / 2; ++t) {
+            if ((t & 7) == 0 && 2 * t >= nrem16) break;
+            const uint32_t ix = static_cast<uint32_t>(__shfl_sync(0xffffffffu, q.idx[t >> 4], (2 * t + hrow) & 31));
+            const uint32_t dst = stg + dst_off[t & 3] + (t >> 2) * KBLK_BYTES;
+            if (live)
+                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst),
+                             "l"(row_addr(src_hi, ix, W2)), "l"(pol)
+                             : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(landed + 8u * s) : "memory");
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 2);
+        it += ngath;
+    }
+}
+
+#ifndef CMF_SCALE_BATCH
+#define CMF_SCALE_BATCH 1
+#endif
+template <int NST, int NBUF>
+__device__ void scale_weighted(const GatherArgs &g, int W, float alpha, const Pipe<NST, true, NBUF> &pp,
+                               uint32_t landed, int pw, int nscal, int lane, int64_t row0, int64_t rstride) {
+    constexpr int SB = CMF_SCALE_BATCH;
+    StageIter cur{0, 0, 0, g.nrows, rstride, &g};
+    cur.first(row0);
+    cur.advance(pw);
+    const int c = lane & 15, hrow = lane >> 4;
+    const bool live = c < (W >> 3);
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int t4 = 0; t4 < 4; ++t4) dst_off[t4] = operand_addr(0, 2 * t4 + hrow, c);
+    uint32_t r_off[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) r_off[h] = operand_addr(0, 32 * h + lane, W >> 3);
+    uint32_t it = pw;
+    StagePairs qn;
+    qn.load(g, cur, lane);
+    while (cur.valid()) {
+        const float pv0 = qn.val[0], pv1 = qn.val[1];
+        const int n16 = static_cast<int>(min(static_cast<int64_t>(KS), cur.p1 - cur.q0) + 15) & ~15;
+        cur.advance(nscal);
+        qn.load(g, cur, lane);
+        const int s = it % NST;
+        const uint32_t stg = pp.stage(s), wst = stg + STAGE_BYTES;
+        // the slot's previous stage (it - NST) consumed first: then landed[s] is at
+        // most one phase ahead of this wait (parity waits alias two phases apart;
+        // valid while nscal <= NST, see the caller)
+        mbar_wait_backoff(pp.empty(s), ((it / NST) & 1) ^ 1);
+        mbar_wait(landed + 8u * s, (it / NST) & 1);  // the gathered rows of stage it are in
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 5);
+        // SB row pairs at a time: all loads first, then the
+        // products and stores (a load -> multiply -> store chain per chunk would
+        // serialise on the shared-memory latency)
+#pragma unroll
+        for (int t0 = 0; t0 < KS / 2; t0 += SB) {
+            if ((t0 & 7) == 0 && 2 * t0 >= n16) break;
+            uint4 v[SB];
+#pragma unroll
+            for (int k = 0; k < SB; ++k) {
+                const uint32_t off = dst_off[k & 3] + ((t0 + k) >> 2) * KBLK_BYTES;
+                if (live)
+                    asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                        : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
+                        : "r"(stg + off));
+            }
+#pragma unroll
+            for (int k = 0; k < SB; ++k) {
+                const int t = t0 + k;
+                const float r = __shfl_sync(0xffffffffu, t < 16 ? pv0 : pv1, (2 * t + hrow) & 31);
+                const __half2 w2 = __float2half2_rn(alpha * r);
+                if (live) {
+                    const uint32_t off = dst_off[k & 3] + (t >> 2) * KBLK_BYTES;
+                    const uint32_t w = *reinterpret_cast<const uint32_t *>(&w2);
+                    auto mul = [&](uint32_t x) {
+                        __half2 y =
+                            __hmul2(*reinterpret_cast<const __half2 *>(&x), *reinterpret_cast<const __half2 *>(&w));
+                        return *reinterpret_cast<const uint32_t *>(&y);
+                    };
+                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(wst + off), "r"(mul(v[k].x)),
+                                 "r"(mul(v[k].y)), "r"(mul(v[k].z)), "r"(mul(v[k].w))
+                                 : "memory");
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float wv = alpha * (h ? pv1 : pv0);
+            const float cv = 1.0f + wv;
+            if ((fabsf(wv) >= 65520.0f || fabsf(cv) >= 65520.0f) && g.overflow) *g.overflow = 1;
+            const __half hi = __float2half_rn(cv);
+            const __half lo = __float2half_rn(cv - __half2float(hi));
+            const uint32_t v = static_cast<uint32_t>(__half_as_ushort(hi)) |
+                               (static_cast<uint32_t>(__half_as_ushort(lo)) << 16);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(wst + r_off[h]), "r"(v) : "memory");
+        }
+        fence_proxy_async();  // generic-proxy stores -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pp.full(s));
+        if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 6);
+        it += nscal;
+    }
+}
+
 __device__ __forceinline__ uint32_t elect_one() {
     uint32_t pred = 0;
     asm volatile(
@@ -423,7 +567,7 @@ __device__ __forceinline__ uint32_t elect_one() {
 // MMA per 16-row K-step; releases stages with tcgen05.commit.  Buffer b
 // occupies columns [b*N, (b+1)*N).  The next row's extent is loaded one row
 // ahead so the indptr latency stays off the issue loop.
-template <int NST, bool SPLIT, int NBUF>
+template <int NST, bool SPLIT, int NBUF, bool WEIGHTED = false>
 __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, SPLIT, NBUF> &pp, uint32_t tmem_base,
                                           int N, int64_t row0, int64_t rstride, uint32_t cons_full = 0,
                                           int ncons = 0) {
@@ -463,6 +607,10 @@ __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, S
                 if (elect_one()) {
                     for (int kk = 0; kk < nk; ++kk) {
                         const uint64_t d = ds + kk * kKStep;
+                        if (WEIGHTED) {  // gathered rows x weighted copy (+ the confidence rows)
+                            tc_mma(tmem_d, d, d + kLoStep, idesc, acc | kk);
+                            continue;
+                        }
                         tc_mma(tmem_d, d, d, idesc, acc | kk);
                         if (SPLIT) {  // + H L^T + L H^T
                             tc_mma(tmem_d, d, d + kLoStep, idesc, 1);

@@ -395,6 +395,35 @@ def implicit_small(cmf):
     np.savez_compressed(os.path.join(OUT, "implicit_small.npz"), **out)
 
 
+def implicit16(cmf):
+    """implicit_train on the implicit_small instance with binary16 Hermitian
+    storage (cg16), alpha = 1 so that alpha r F^T F stays inside binary16 range;
+    plus one cg16 implicit_update_side from x0 (rows without observations
+    included)."""
+    import cmf.implicit as imp
+    g = dict(np.load(os.path.join(OUT, "implicit_small.npz")))
+    m, n, f = (int(v) for v in g["meta"])
+    sr = cmf.SparseRatings(m, n, int(g["row_ptr"][-1]), g["row_ptr"], g["col_idx"], g["csr_val"],
+                           g["col_ptr"], g["row_idx"], g["csc_val"])
+    te = cmf.Triples(g["te_u"], g["te_v"], g["te_r"])
+    out = {"meta": g["meta"], "alpha": np.array(1.0)}
+    cfg = cmf.SolverConfig("cg", 6, 1e-4, "fp16")
+    theta = cmf.init_factors(n, f, 0.1, [0, 1])
+    x1 = g["x0"].copy()
+    imp.implicit_update_side(sr.csr_view(), theta, imp.precompute_gram(theta), x1, 1.0, 0.05, cfg)
+    out["x1_cg16"] = x1
+    X, T, rep = imp.implicit_train(sr, imp.ImplicitConfig(f=f, alpha=1.0, lam=0.05, epochs=4, solver=cfg), te)
+    out["cg16_X"], out["cg16_T"] = X, T
+    out["cg16_obj"] = np.array([e.objective for e in rep.epochs])
+    out["cg16_rmse"] = np.array([e.rmse for e in rep.epochs])
+    X, T, rep = imp.implicit_train(sr, imp.ImplicitConfig(f=f, alpha=1.0, lam=0.05, epochs=4,
+                                                          solver=cmf.SolverConfig("exact")), te)
+    out["exact_obj"] = np.array([e.objective for e in rep.epochs])
+    out["exact_rmse"] = np.array([e.rmse for e in rep.epochs])
+    print("implicit16", out["cg16_obj"], out["cg16_rmse"], out["exact_rmse"])
+    np.savez_compressed(os.path.join(OUT, "implicit16.npz"), **out)
+
+
 def io_cases(cmf):
     out = {}
     rng = np.random.default_rng(21)
@@ -427,5 +456,5 @@ if __name__ == "__main__":
     for w in which:
         {"gram": gram_cases, "solve": solve_cases, "build": build_cases,
          "data": data_cases, "small": train_small, "implicit": implicit_small,
-         "io": io_cases, "ml1m": train_ml1m, "f100": train_f100}[w](cmf)
+         "io": io_cases, "ml1m": train_ml1m, "f100": train_f100, "implicit16": implicit16}[w](cmf)
         print("wrote", w)

@@ -83,3 +83,52 @@ def test_implicit_fp16_overflow_and_negative_ratings(golden, cuda_device):
                              sr.row_idx, -sr.csc_val)
     with pytest.raises(cmfb.DataError):
         cmfb.implicit_train(bad, cfg, te)
+
+
+def test_implicit_fused_tc_route_vs_reference(golden, cuda_device):
+    """cg16 implicit (binary16 Hermitian storage) runs on the fused tensor-core
+    kernel with per-rating operand weights (cmf_fused_cg_update_implicit): the
+    reference's own cg16 trajectory (tests/golden/implicit16.npz, alpha = 1)
+    within the north_star's 1e-3 RMSE bar; rows without observations solved."""
+    from paper_1808_03843_b200 import _native as nat
+    g16 = golden("implicit16")
+    g = golden("implicit_small")
+    sr, te, f = _instance(g)
+    cfg = cmfb.SolverConfig("cg", 6, 1e-4, "fp16")
+    theta = cmfb.init_factors(sr.n, f, 0.1, [0, 1])
+    x = g["x0"].copy()
+    n0 = nat.LAUNCHES[0]
+    cmfb.implicit_update_side(sr.csr_view(), theta, cmfb.precompute_gram(theta), x, 1.0, 0.05, cfg)
+    assert nat.LAUNCHES[0] > n0
+    # fp16 operands: the half-update agrees with the reference's fp16 route to ~1e-3
+    assert _rel(x, g16["x1_cg16"]) < 5e-3
+    X, T, rep = cmfb.implicit_train(sr, cmfb.ImplicitConfig(f=f, alpha=1.0, lam=0.05, epochs=4, solver=cfg), te)
+    rmse = np.array([e.rmse for e in rep.epochs])
+    obj = np.array([e.objective for e in rep.epochs])
+    assert np.abs(rmse - g16["cg16_rmse"]).max() < 1e-3
+    assert np.allclose(obj, g16["cg16_obj"], rtol=1e-3)
+
+
+def test_implicit_fused_matches_two_step(golden, cuda_device):
+    """Same half-update through the fused weighted kernel and through the
+    reference-layout two-step route (fp32 weighted Gram -> fp16 pack -> CG on
+    the same binary16 systems): the fused kernel's fp16 operand rounding is the
+    only difference (f = 100, every row long enough for several K-chunks)."""
+    import torch
+    rng = np.random.default_rng(5)
+    m, n, f = 600, 900, 100
+    k = 60_000
+    u = rng.integers(0, m, k)
+    v = rng.integers(0, n, k)
+    r = rng.integers(1, 6, k).astype(np.float32)
+    sr = cmfb.build(cmfb.Triples(u, v, r), m + 3, n)  # three empty rows
+    theta = cmfb.init_factors(n, f, 0.1, [0, 1])
+    gram = cmfb.precompute_gram(theta)
+    x0 = cmfb.init_factors(m + 3, f, 0.1, [0, 0])
+    xa = x0.copy()
+    cmfb.implicit_update_side(sr.csr_view(), theta, gram, xa, 0.5, 0.05, cmfb.SolverConfig("cg", 6, 1e-4, "fp16"))
+    xb = x0.copy()
+    cmfb.implicit_update_side(sr.csr_view(), theta, gram, xb, 0.5, 0.05, cmfb.SolverConfig("cg", 6, 1e-4, "fp16"),
+                              gram_kernel="fma")
+    assert _rel(xa, xb) < 5e-3
+    assert np.all(np.isfinite(xa[-3:])) and np.abs(xa[-3:]).max() < np.abs(x0[-3:]).max()
