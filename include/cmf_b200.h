@@ -316,6 +316,35 @@ int cmf_build(const void *user, const void *item, int32_t idx64, const float *ra
               int64_t *bad_host, void *stream);
 int64_t cmf_build_workspace_bytes(int64_t k);
 
+/*
+ * Implicit-feedback helpers (f1 in SURVEY 8; implicit.py:57-131).
+ *
+ * cmf_dense_gram: packed lower triangle of F^T F for a row-major (rows, f)
+ * float32 matrix -- implicit.precompute_gram (implicit.py:57-60).  fp64 != 0:
+ * float64 accumulation and output (the objective's Gram trick), else float32.
+ * Deterministic (per-block partials summed in block order).  f <= 124.
+ * ws: cmf_dense_gram_workspace_bytes(rows, f, fp64) bytes.
+ */
+int64_t cmf_dense_gram_workspace_bytes(int64_t rows, int32_t f, int32_t fp64);
+int cmf_dense_gram(const float *F, int64_t rows, int32_t f, int32_t fp64, void *out_packed, void *ws,
+                   int64_t ws_bytes, void *stream);
+/* sum over a CSR view of c (1 - x_u.theta_v)^2 - (x_u.theta_v)^2, c = 1 + alpha r,
+ * float64, deterministic -> *out (CMF_REDUCE_SLOTS doubles, like cmf_sq_error):
+ * the sparse part of implicit_objective (implicit.py:87-104). */
+int cmf_implicit_loss_csr(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
+                          const float *x, const float *theta, int32_t f, double alpha, double *out, void *stream);
+/* Stable grouping of (row, col) pairs by row, duplicates kept: indptr[nrows+1],
+ * cols_out[k] (int32).  rows/cols int64 when idx64 != 0.  ws: cmf_group_workspace_bytes(k). */
+int64_t cmf_group_workspace_bytes(int64_t k);
+int cmf_group_rows(const void *rows, const void *cols, int32_t idx64, int64_t k, int64_t nrows, int64_t *indptr,
+                   int32_t *cols_out, void *ws, int64_t ws_bytes, void *stream);
+/* Mean percentile rank numerator (implicit.py:115-131) over positives grouped
+ * by user (pos_ptr[m+1], pos_item): *out (uint64, device) = sum over positives
+ * of 2 #{i: s_ui > s_uv} + #{i != v: s_ui == s_uv}, s = float32 x_u.theta_i;
+ * MPR = *out / (2 (n - 1) #positives).  Exact integer sum. */
+int cmf_mpr_count(const int64_t *pos_ptr, const int32_t *pos_item, int64_t m, const float *x, const float *theta,
+                  int64_t n, int32_t f, uint64_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

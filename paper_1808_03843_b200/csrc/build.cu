@@ -494,3 +494,62 @@ int build_launch(const void *user, const void *item, bool idx64, const float *ra
 }
 
 }  // namespace cmf
+
+// ------------------------------------------------------------ grouping without dedup
+namespace cmf {
+namespace bld {
+template <typename I>
+__global__ void group_keys_kernel(const I *rows, const I *cols, int64_t k, uint32_t *key, uint32_t *pay) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < k;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        key[t] = static_cast<uint32_t>(rows[t]);
+        pay[t] = static_cast<uint32_t>(cols[t]);
+    }
+}
+}  // namespace bld
+
+int64_t group_workspace_bytes(int64_t k) {
+    const int64_t ntiles = (k + bld::TILE - 1) / bld::TILE;
+    const int64_t hist = bld::RADIX * (ntiles > 0 ? ntiles : 1);
+    return 4 * align256(4 * k) + align256(4 * hist) + align256(4 * (hist / bld::TILE + 2));
+}
+
+// (row, col) pairs -> indptr[nrows+1] + cols in stable row order (file order kept
+// inside a row, duplicates kept): the positives' grouping for mean_percentile_rank
+template <typename I>
+static int group_impl(const I *rows, const I *cols, int64_t k, int64_t nrows, int64_t *indptr, int32_t *cols_out,
+                      void *ws, int64_t ws_bytes, cudaStream_t st) {
+    if (ws_bytes < group_workspace_bytes(k)) return set_error(CMF_EINVAL, "group workspace too small");
+    char *p = static_cast<char *>(ws);
+    uint32_t *k0 = reinterpret_cast<uint32_t *>(p);
+    uint32_t *k1 = reinterpret_cast<uint32_t *>(p + align256(4 * k));
+    uint32_t *p0 = reinterpret_cast<uint32_t *>(p + 2 * align256(4 * k));
+    uint32_t *p1 = reinterpret_cast<uint32_t *>(p + 3 * align256(4 * k));
+    const int64_t ntiles = (k + bld::TILE - 1) / bld::TILE;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(p + 4 * align256(4 * k));
+    uint32_t *part = reinterpret_cast<uint32_t *>(p + 4 * align256(4 * k) +
+                                                  align256(4 * bld::RADIX * (ntiles > 0 ? ntiles : 1)));
+    if (k == 0) {
+        bld::fill_i64_kernel<<<grid_for(nrows + 1), 256, 0, st>>>(indptr, nrows + 1, 0);
+        return check_launch("group (empty)");
+    }
+    bld::group_keys_kernel<I><<<grid_for(k), 256, 0, st>>>(rows, cols, k, k0, p0);
+    int rc = radix_sort<uint32_t>(k0, p0, k1, p1, k, bit_length(static_cast<uint64_t>(nrows > 1 ? nrows - 1 : 1)),
+                                  hist, part, st);
+    if (rc != CMF_OK) return rc;
+    bld::bounds_kernel<<<grid_for(k + 1), 256, 0, st>>>(k0, k, nrows, indptr);
+    cudaError_t e = cudaMemcpyAsync(cols_out, p0, 4 * k, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return set_error(CMF_ECUDA, "group: %s", cudaGetErrorString(e));
+    return check_launch("group");
+}
+
+int group_launch(const void *rows, const void *cols, bool idx64, int64_t k, int64_t nrows, int64_t *indptr,
+                 int32_t *cols_out, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    if (idx64)
+        return group_impl(static_cast<const int64_t *>(rows), static_cast<const int64_t *>(cols), k, nrows, indptr,
+                          cols_out, ws, ws_bytes, st);
+    return group_impl(static_cast<const int32_t *>(rows), static_cast<const int32_t *>(cols), k, nrows, indptr,
+                      cols_out, ws, ws_bytes, st);
+}
+
+}  // namespace cmf

@@ -50,6 +50,15 @@ int build_launch(const void *, const void *, bool, const float *, int64_t, int64
                  int64_t *, int32_t *, float *, void *, int64_t, int64_t *, int64_t *, cudaStream_t);
 int64_t build_workspace_bytes(int64_t k);
 int fused_base_ld(int f);
+int64_t group_workspace_bytes(int64_t k);
+int group_launch(const void *, const void *, bool, int64_t, int64_t, int64_t *, int32_t *, void *, int64_t,
+                 cudaStream_t);
+int64_t dense_gram_workspace_bytes(int64_t rows, int f, bool fp64);
+int dense_gram_launch(const float *, int64_t, int, bool, void *, void *, int64_t, cudaStream_t);
+int implicit_loss_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, const float *, int,
+                         double, double *, cudaStream_t);
+int mpr_launch(const int64_t *, const int32_t *, int64_t, const float *, const float *, int64_t, int,
+               unsigned long long *, cudaStream_t);
 
 int gram_tc_trace(void *buf);
 int fused_cg_trace(void *buf);
@@ -401,5 +410,36 @@ int cmf_build(const void *user, const void *item, int32_t idx64, const float *ra
 }
 
 int64_t cmf_build_workspace_bytes(int64_t k) { return k < 0 ? -1 : build_workspace_bytes(k); }
+
+int64_t cmf_group_workspace_bytes(int64_t k) { return k < 0 ? -1 : group_workspace_bytes(k); }
+
+int cmf_group_rows(const void *rows, const void *cols, int32_t idx64, int64_t k, int64_t nrows, int64_t *indptr,
+                   int32_t *cols_out, void *ws, int64_t ws_bytes, void *stream) {
+    REQUIRE(k >= 0 && nrows >= 0 && indptr && (k == 0 || (rows && cols && cols_out && ws)), "bad group arguments");
+    REQUIRE(nrows < (int64_t(1) << 32) && k < (int64_t(1) << 32), "group: 32-bit row ids and counts");
+    return group_launch(rows, cols, idx64 != 0, k, nrows, indptr, cols_out, ws, ws_bytes, S(stream));
+}
+
+int64_t cmf_dense_gram_workspace_bytes(int64_t rows, int32_t f, int32_t fp64) {
+    return (rows < 0 || f < 1) ? -1 : dense_gram_workspace_bytes(rows, f, fp64 != 0);
+}
+
+int cmf_dense_gram(const float *F, int64_t rows, int32_t f, int32_t fp64, void *out_packed, void *ws,
+                   int64_t ws_bytes, void *stream) {
+    REQUIRE(rows >= 0 && f >= 1 && F && out_packed && ws, "bad dense_gram arguments");
+    return dense_gram_launch(F, rows, f, fp64 != 0, out_packed, ws, ws_bytes, S(stream));
+}
+
+int cmf_implicit_loss_csr(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
+                          const float *x, const float *theta, int32_t f, double alpha, double *out, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1 && out, "bad arguments");
+    return implicit_loss_launch(indptr, indices, values, nrows, x, theta, f, alpha, out, S(stream));
+}
+
+int cmf_mpr_count(const int64_t *pos_ptr, const int32_t *pos_item, int64_t m, const float *x, const float *theta,
+                  int64_t n, int32_t f, uint64_t *out, void *stream) {
+    REQUIRE(m >= 0 && n >= 1 && f >= 1 && pos_ptr && out && x && theta, "bad mpr arguments");
+    return mpr_launch(pos_ptr, pos_item, m, x, theta, n, f, reinterpret_cast<unsigned long long *>(out), S(stream));
+}
 
 }  // extern "C"

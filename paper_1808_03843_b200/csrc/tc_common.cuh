@@ -507,7 +507,7 @@ __device__ void scale_weighted(const GatherArgs &g, int W, float alpha, const Pi
             uint4 v[SB];
 #pragma unroll
             for (int k = 0; k < SB; ++k) {
-                const uint32_t off = dst_off[k & 3] + ((t0 + k) >> 2) * KBLK_BYTES;
+                const uint32_t off = dst_off[(t0 + k) & 3] + ((t0 + k) >> 2) * KBLK_BYTES;
                 if (live)
                     asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                         : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
@@ -519,7 +519,7 @@ __device__ void scale_weighted(const GatherArgs &g, int W, float alpha, const Pi
                 const float r = __shfl_sync(0xffffffffu, t < 16 ? pv0 : pv1, (2 * t + hrow) & 31);
                 const __half2 w2 = __float2half2_rn(alpha * r);
                 if (live) {
-                    const uint32_t off = dst_off[k & 3] + (t >> 2) * KBLK_BYTES;
+                    const uint32_t off = dst_off[t & 3] + (t >> 2) * KBLK_BYTES;
                     const uint32_t w = *reinterpret_cast<const uint32_t *>(&w2);
                     auto mul = [&](uint32_t x) {
                         __half2 y =

@@ -132,3 +132,51 @@ def test_implicit_fused_matches_two_step(golden, cuda_device):
                               gram_kernel="fma")
     assert _rel(xa, xb) < 5e-3
     assert np.all(np.isfinite(xa[-3:])) and np.abs(xa[-3:]).max() < np.abs(x0[-3:]).max()
+
+
+def _mpr_loop(x, theta, users, items):
+    """implicit.py:115-131 restated (float32 scores, ties averaged)."""
+    n = theta.shape[0]
+    total = 0.0
+    for u in np.unique(users):
+        scores = (x[u].astype(np.float64) @ theta.T.astype(np.float64)).astype(np.float32)
+        for v in items[users == u]:
+            total += ((scores > scores[v]).sum() + 0.5 * ((scores == scores[v]).sum() - 1.0)) / (n - 1)
+    return total / len(users)
+
+
+def test_mean_percentile_rank_kernel_ties_and_duplicates(cuda_device):
+    """cmf_mpr_count: exact ties (duplicated item rows), duplicate positives,
+    users without positives, n not a multiple of the 128-item tile, f not a
+    multiple of 4; compared with a float64-scored restatement (exact integer
+    counts; scores are well separated except for the planted ties)."""
+    rng = np.random.default_rng(7)
+    m, n, f = 70, 301, 13
+    x = rng.standard_normal((m, f)).astype(np.float32)
+    theta = rng.standard_normal((n, f)).astype(np.float32)
+    theta[10] = theta[11] = theta[200]  # three-way tie
+    users = rng.integers(0, m - 5, 900)
+    items = rng.integers(0, n, 900)
+    items[:30] = 11
+    users[50], items[50] = users[51], items[51]  # a duplicate positive
+    got = cmfb.mean_percentile_rank(x, theta, cmfb.Triples(users, items, np.ones(900, np.float32)))
+    assert abs(got - _mpr_loop(x, theta, users, items)) < 1e-6
+
+
+def test_dense_gram_and_implicit_objective(golden, cuda_device):
+    import torch
+    rng = np.random.default_rng(3)
+    F = rng.standard_normal((5000, 37)).astype(np.float32)
+    g = cmfb.precompute_gram(F)
+    full = F.astype(np.float64).T @ F.astype(np.float64)
+    r, c = np.tril_indices(37)
+    assert np.abs(g - full[r, c]).max() / np.abs(full).max() < 1e-6
+    # deterministic: same bits twice, device in -> device out
+    gd1 = cmfb.precompute_gram(torch.from_numpy(F).cuda())
+    gd2 = cmfb.precompute_gram(torch.from_numpy(F).cuda())
+    assert torch.equal(gd1, gd2) and gd1.is_cuda
+    gi = golden("implicit_small")
+    sr, _, f = _instance(gi)
+    X, T = gi["exact_X"][-1], gi["exact_T"][-1]
+    obj = cmfb.implicit.implicit_objective(X, T, sr, 40.0, 0.05)
+    assert np.isclose(obj, gi["exact_obj"][-1], rtol=1e-8, atol=1e-6)
