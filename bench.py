@@ -40,8 +40,9 @@ SHAPES = {
     "netflix": (480_189, 17_770, 99_000_000),
     "yahoo": (1_000_990, 624_961, 252_800_000),
     "ml1m": (6_040, 3_706, 1_000_000),
+    "hugewiki": (50_082_604, 39_780, 3_100_000_000),
 }
-DATA_DEFAULT = {"netflix": "reference", "ml1m": "reference", "yahoo": "device"}
+DATA_DEFAULT = {"netflix": "reference", "ml1m": "reference", "yahoo": "device", "hugewiki": "stream"}
 SOLVERS = {"cg16": ("cg", "fp16"), "cg32": ("cg", "fp32"), "exact": ("exact", "fp32")}
 
 
@@ -61,7 +62,7 @@ def parse():
     ap.add_argument("--no-ttr", action="store_true", help="skip time-to-RMSE")
     ap.add_argument("--no-next", action="store_true",
                     help="skip the SURVEY 8(f) rows (implicit iteration, eval, build)")
-    ap.add_argument("--data", default=None, choices=["reference", "device"],
+    ap.add_argument("--data", default=None, choices=["reference", "device", "stream"],
                     help="reference: the reference's host generator + split (bit-identical "
                          "inputs; default for netflix / ml1m); device: the fast on-GPU generator")
     return ap.parse_args()
@@ -157,6 +158,8 @@ def workload_label(shape, f, solver, world):
         return base + " (BASELINE configs[1])"
     if shape == "yahoo" and f == 100 and solver == "cg16":
         return base + f" (BASELINE configs[3] shape on {world} GPU{'s' if world > 1 else ''})"
+    if shape == "hugewiki" and f == 100 and solver == "cg16":
+        return base + f" (BASELINE configs[4] shape on {world} GPU{'s' if world > 1 else ''})"
     return base
 
 
@@ -335,6 +338,27 @@ def main():
         data_desc = ("synthetic, the reference protocol (SURVEY 8(d)): gen_synthetic(seed 0, "
                      "sigma 0.1) + split_holdout(0.1, seed 1) on the host, bit-identical to the "
                      "reference's draws; CSR/CSC built per rank on the GPU")
+    elif data_kind == "stream":
+        # every rank generates only its own CSR rows / CSC columns (gen.cu); no triples
+        ub = [s * m // world for s in range(world + 1)]
+        vb = [s * n // world for s in range(world + 1)]
+        sh = cmfb.gen_stream_shard(m, n, f, nnz, 0.1, 0.1, 0, users=(ub[rank], ub[rank + 1]),
+                                   items=(vb[rank], vb[rank + 1]))
+        del sh.x_true, sh.t_true
+        t_host = 0.0
+        test = sh.test
+        local_nnz = int(sh.x_view[1].numel())
+        if world == 1:
+            shards = cmfb.DeviceRatings(m, n, local_nnz, *sh.x_view, *sh.t_view)
+        else:
+            tot = torch.tensor([local_nnz], dtype=torch.int64,
+                               device="cuda" if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(tot)
+            shards = cdist.ShardedRatings(m, n, int(tot.item()), ub, vb, sh.x_view, sh.t_view)
+        del sh
+        data_desc = ("synthetic, streaming generator (gen.cu): counter-based Bernoulli cells, U[-0.5,0.5) "
+                     "rank-f truth, Irwin-Hall noise sigma 0.1, 10% holdout; each rank generates only its "
+                     "CSR rows and CSC columns on its GPU (row-balanced ranges)")
     else:
         train_full, test = cmfb.gen_synthetic_device(m, n, f, nnz, 0.1, 0.1, seed=0)
         t_host = 0.0
@@ -401,7 +425,13 @@ def main():
     ms = ms_total / args.steps
     sec = ms / 1e3
     engine.check()
-    test_rmse = cmfb.rmse(x, th, test)
+    if data_kind == "stream" and world > 1:  # each rank holds its own users' test triples
+        sse = torch.tensor([cmfb.rmse(x, th, test) ** 2 * len(test), float(len(test))], dtype=torch.float64,
+                           device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(sse)
+        test_rmse = float((sse[0] / sse[1]).sqrt())
+    else:
+        test_rmse = cmfb.rmse(x, th, test)
 
     # ---- per-kernel device time inside the timed region -> roofline of the dominant kernel
     P = f * (f + 1) // 2
@@ -480,6 +510,10 @@ def main():
     result["clocks"] = clk.summary()
 
     # ---- configs[1]: exact Cholesky on the same data
+    if data_kind == "stream":  # host-side legs (e2e copies, oracle CPU run, exact route) do not scale there
+        args.no_exact = args.no_e2e = args.no_cpu = args.no_ttr = args.no_next = True
+        result["note_stream"] = ("streamed shards: e2e / cpu_baseline / exact / time-to-RMSE legs skipped "
+                                 "(they need the whole matrix on the host)")
     if not args.no_exact and method != "exact":
         ex_engine = cdist.ShardedALS(shards, f, lam=0.05, solver=cmfb.SolverConfig("exact"),
                                      gram_kernel="auto", rank=rank, world=world)

@@ -345,6 +345,31 @@ int cmf_group_rows(const void *rows, const void *cols, int32_t idx64, int64_t k,
 int cmf_mpr_count(const int64_t *pos_ptr, const int32_t *pos_item, int64_t m, const float *x, const float *theta,
                   int64_t n, int32_t f, uint64_t *out, void *stream);
 
+/*
+ * Streaming synthetic generator (f3 in SURVEY 8; a counter-based restatement
+ * of gen_synthetic's model, data.py:270-302, that any rank evaluates for its
+ * own shard).  Cell (u, v) is present iff H(s_cell, u, v) < thr_cell, held out
+ * iff also H(s_test, u, v) < thr_test; truth X / Theta entries and the rating
+ * noise are hashes of (seed, index) too (gen.cu header).  Three calls:
+ *   cmf_gen_truth:  which = 0 -> X (rows = m), 1 -> Theta (rows = n), (rows, f) float32;
+ *   cmf_gen_count:  majors [lo, hi) (users when by_user != 0, else items) ->
+ *                   ptr[hi-lo+1] (train cells per major, exclusive scan; ptr[hi-lo] = total)
+ *                   and, for users only, tptr (test cells, nullable);
+ *                   scratch: 2 (hi - lo) int64;
+ *   cmf_gen_fill:   minor ids (ascending: build() order) and ratings of the
+ *                   train cells at ptr; with tptr, the test triples (int64
+ *                   user, item; float32 rating) of those users at tptr.
+ * by_user = 1 gives a CSR shard, 0 a CSC shard; concatenated shards equal
+ * data.build of the generated triples byte for byte (tests/test_gpu_gen.py).
+ */
+int cmf_gen_truth(uint64_t seed, int32_t which, int64_t rows, int32_t f, float *out, void *stream);
+int cmf_gen_count(uint64_t seed, int64_t m, int64_t n, uint64_t thr_cell, uint64_t thr_test, int32_t by_user,
+                  int64_t lo, int64_t hi, int64_t *ptr, int64_t *tptr, int64_t *scratch, void *stream);
+int cmf_gen_fill(uint64_t seed, int64_t m, int64_t n, int32_t f, uint64_t thr_cell, uint64_t thr_test,
+                 float noise_scale, int32_t by_user, int64_t lo, int64_t hi, const float *X, const float *T,
+                 const int64_t *ptr, int32_t *minor_out, float *val_out, const int64_t *tptr, int64_t *test_u,
+                 int64_t *test_v, float *test_r, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

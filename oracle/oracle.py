@@ -176,6 +176,55 @@ def build(t: OTriples, m: int, n: int) -> ORatings:
                     sv[co].astype(np.float32))
 
 
+def _mix64(z):
+    """splitmix64 finaliser on uint64 arrays (wrap-around arithmetic), gen.cu mix64."""
+    z = np.asarray(z, dtype=np.uint64)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+    return z ^ (z >> np.uint64(31))
+
+
+def gen_stream_triples(seed, m, n, f, thr_cell, thr_test, noise_scale):
+    """numpy restatement of the streaming generator (paper_1808_03843_b200
+    csrc/gen.cu -- the B200 package's own counter-based generator, a restatement
+    of gen_synthetic's model, data.py:270-302; not the reference's PCG64 draws):
+    returns (train triples, test triples) in (user, item) order.  Small m*n only
+    (every cell is hashed)."""
+    with np.errstate(over="ignore"):
+        base = np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15)
+        salts = [_mix64(base + np.uint64(k)) for k in range(1, 6)]
+        s_cell, s_test, s_noise, s_x, s_t = salts
+
+        def H(s, a, b):
+            return _mix64(((np.asarray(a, np.uint64) << np.uint64(32)) | np.asarray(b, np.uint64)) ^ s)
+
+        def truth(salt, rows):
+            r, k = np.meshgrid(np.arange(rows, dtype=np.uint64), np.arange(f, dtype=np.uint64), indexing="ij")
+            v = (H(salt, r, k) >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -24)
+            return (v - np.float32(0.5)).astype(np.float32)
+
+        X, T = truth(s_x, m), truth(s_t, n)
+        uu, vv = np.meshgrid(np.arange(m, dtype=np.uint64), np.arange(n, dtype=np.uint64), indexing="ij")
+        uu, vv = uu.ravel(), vv.ravel()
+        present = H(s_cell, uu, vv) < np.uint64(thr_cell)
+        uu, vv = uu[present], vv[present]
+        test = H(s_test, uu, vv) < np.uint64(thr_test)
+        acc = np.zeros(uu.shape[0], np.float32)
+        xi, ti = X[uu.astype(np.int64)], T[vv.astype(np.int64)]
+        for k in range(f):  # sequential, round after every multiply and add
+            acc = (acc + (xi[:, k] * ti[:, k]).astype(np.float32)).astype(np.float32)
+        h = H(s_noise, uu, vv)
+        q = [((h >> np.uint64(sh)) & np.uint64(0xffff)).astype(np.float32) for sh in (0, 16, 32, 48)]
+        q = [((x + np.float32(0.5)) * np.float32(2.0 ** -16)).astype(np.float32) for x in q]
+        s = ((q[0] + q[1]).astype(np.float32) + (q[2] + q[3]).astype(np.float32)).astype(np.float32)
+        s = (s - np.float32(2.0)).astype(np.float32)
+        r = (acc + (s * np.float32(noise_scale)).astype(np.float32)).astype(np.float32)
+    u64, v64 = uu.astype(np.int64), vv.astype(np.int64)
+    tr = OTriples(u64[~test], v64[~test], r[~test])
+    te = OTriples(u64[test], v64[test], r[test])
+    return tr, te, X, T
+
+
 def init_factors(rows, f, scale=0.1, seed=0):
     """factors.py:29-38."""
     raw = np.random.default_rng(seed).random((rows, f), dtype=np.float32)

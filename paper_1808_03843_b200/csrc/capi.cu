@@ -50,6 +50,12 @@ int build_launch(const void *, const void *, bool, const float *, int64_t, int64
                  int64_t *, int32_t *, float *, void *, int64_t, int64_t *, int64_t *, cudaStream_t);
 int64_t build_workspace_bytes(int64_t k);
 int fused_base_ld(int f);
+int gen_truth_launch(uint64_t, int, int64_t, int, float *, cudaStream_t);
+int gen_count_launch(uint64_t, int64_t, int64_t, uint64_t, uint64_t, int, int64_t, int64_t, int64_t *, int64_t *,
+                     int64_t *, cudaStream_t);
+int gen_fill_launch(uint64_t, int64_t, int64_t, int, uint64_t, uint64_t, float, int, int64_t, int64_t, const float *,
+                    const float *, const int64_t *, int32_t *, float *, const int64_t *, int64_t *, int64_t *, float *,
+                    cudaStream_t);
 int64_t group_workspace_bytes(int64_t k);
 int group_launch(const void *, const void *, bool, int64_t, int64_t, int64_t *, int32_t *, void *, int64_t,
                  cudaStream_t);
@@ -410,6 +416,32 @@ int cmf_build(const void *user, const void *item, int32_t idx64, const float *ra
 }
 
 int64_t cmf_build_workspace_bytes(int64_t k) { return k < 0 ? -1 : build_workspace_bytes(k); }
+
+int cmf_gen_truth(uint64_t seed, int32_t which, int64_t rows, int32_t f, float *out, void *stream) {
+    REQUIRE(rows >= 0 && f >= 1 && (which == 0 || which == 1) && (rows == 0 || out), "bad gen_truth arguments");
+    REQUIRE(rows < (int64_t(1) << 32), "gen: 32-bit row ids");
+    return gen_truth_launch(seed, which, rows, f, out, S(stream));
+}
+
+int cmf_gen_count(uint64_t seed, int64_t m, int64_t n, uint64_t thr_cell, uint64_t thr_test, int32_t by_user,
+                  int64_t lo, int64_t hi, int64_t *ptr, int64_t *tptr, int64_t *scratch, void *stream) {
+    REQUIRE(m >= 0 && n >= 0 && m < (int64_t(1) << 32) && n < (int64_t(1) << 31), "gen: bad extents");
+    REQUIRE(lo >= 0 && hi >= lo && hi <= (by_user ? m : n), "gen: bad major range");
+    REQUIRE(ptr && (hi == lo || scratch), "null argument");
+    return gen_count_launch(seed, m, n, thr_cell, thr_test, by_user, lo, hi, ptr, tptr, scratch, S(stream));
+}
+
+int cmf_gen_fill(uint64_t seed, int64_t m, int64_t n, int32_t f, uint64_t thr_cell, uint64_t thr_test,
+                 float noise_scale, int32_t by_user, int64_t lo, int64_t hi, const float *X, const float *T,
+                 const int64_t *ptr, int32_t *minor_out, float *val_out, const int64_t *tptr, int64_t *test_u,
+                 int64_t *test_v, float *test_r, void *stream) {
+    REQUIRE(m >= 0 && n >= 0 && m < (int64_t(1) << 32) && n < (int64_t(1) << 31) && f >= 1, "gen: bad extents");
+    REQUIRE(lo >= 0 && hi >= lo && hi <= (by_user ? m : n), "gen: bad major range");
+    REQUIRE(X && T && ptr, "null argument");
+    REQUIRE(!tptr || (by_user && test_u && test_v && test_r), "test triples come from the user pass");
+    return gen_fill_launch(seed, m, n, f, thr_cell, thr_test, noise_scale, by_user, lo, hi, X, T, ptr, minor_out,
+                           val_out, tptr, test_u, test_v, test_r, S(stream));
+}
 
 int64_t cmf_group_workspace_bytes(int64_t k) { return k < 0 ? -1 : group_workspace_bytes(k); }
 

@@ -372,6 +372,91 @@ def _host_dot(x, t, users, items, chunk=1 << 18):
     return out
 
 
+def stream_params(m: int, n: int, nnz: int, noise_sigma: float = 0.1, test_fraction: float = 0.1):
+    """Integer Bernoulli thresholds and the float32 noise scale of the streaming
+    generator: cells present with p = nnz / (1 - test_fraction) / (m n), held out
+    with q = test_fraction (so the expected train count is nnz)."""
+    if m < 1 or n < 1 or nnz < 1:
+        raise DataError("streaming generator needs m, n, nnz >= 1")
+    if not (0.0 <= test_fraction < 1.0):
+        raise DataError(f"test_fraction must be in [0, 1), got {test_fraction}")
+    p = nnz / (1.0 - test_fraction) / (float(m) * float(n))
+    if p > 1.0:
+        raise DataError(f"{nnz} ratings do not fit a {m}x{n} matrix")
+    thr_cell = min(int(p * 2.0 ** 64), 2 ** 64 - 1)
+    thr_test = min(int(test_fraction * 2.0 ** 64), 2 ** 64 - 1)
+    scale = float(np.float32(noise_sigma * math.sqrt(3.0)))
+    return thr_cell, thr_test, scale
+
+
+@dataclass
+class StreamShard:
+    """One rank's generated shards: CSR rows of users [u0, u1) and CSC rows of
+    items [v0, v1) (pointers rebased to the shard), the held-out triples of its
+    users, and the truth factors the ratings were drawn from."""
+    m: int
+    n: int
+    users: tuple
+    items: tuple
+    x_view: tuple
+    t_view: tuple
+    test: Triples
+    x_true: torch.Tensor
+    t_true: torch.Tensor
+
+
+def gen_stream_shard(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1, test_fraction: float = 0.1,
+                     seed: int = 0, users: tuple | None = None, items: tuple | None = None) -> StreamShard:
+    """Streaming synthetic generator (gen.cu): the CSR rows of
+    users [u0, u1) and CSC rows of items [v0, v1) of a low-rank-plus-noise
+    matrix with ~nnz train ratings, generated on the device in build() order
+    from counter-based hashes -- no triples are materialised, no rank sees
+    another's shard, and the shards of all ranks tile the global matrix.  The
+    model is gen_synthetic's (data.py:270-302: U[-1/2, 1/2) truth, uniformly
+    random cells, dot + noise of variance sigma^2) but its draws are not the
+    reference's PCG64 stream (Bernoulli cells, Irwin-Hall noise)."""
+    u0, u1 = users if users is not None else (0, m)
+    v0, v1 = items if items is not None else (0, n)
+    thr_cell, thr_test, scale = stream_params(m, n, nnz, noise_sigma, test_fraction)
+    dev = nat.device()
+    st = nat.stream_ptr()
+    X = torch.empty(m, f, dtype=torch.float32, device=dev)
+    T = torch.empty(n, f, dtype=torch.float32, device=dev)
+    nat.call("cmf_gen_truth", seed, 0, m, f, nat.ptr(X), st)
+    nat.call("cmf_gen_truth", seed, 1, n, f, nat.ptr(T), st)
+
+    def side(by_user, lo, hi):
+        nr = hi - lo
+        ptr = torch.empty(nr + 1, dtype=torch.int64, device=dev)
+        tptr = torch.empty(nr + 1, dtype=torch.int64, device=dev) if by_user else None
+        scratch = torch.empty(max(2 * nr, 1), dtype=torch.int64, device=dev)
+        nat.call("cmf_gen_count", seed, m, n, thr_cell, thr_test, int(by_user), lo, hi, nat.ptr(ptr),
+                 nat.ptr(tptr), nat.ptr(scratch), st)
+        ntr = int(ptr[-1].item())
+        nte = int(tptr[-1].item()) if by_user else 0
+        minor = torch.empty(ntr, dtype=torch.int32, device=dev)
+        val = torch.empty(ntr, dtype=torch.float32, device=dev)
+        tu = torch.empty(nte, dtype=torch.int64, device=dev) if by_user else None
+        tv = torch.empty(nte, dtype=torch.int64, device=dev) if by_user else None
+        tr = torch.empty(nte, dtype=torch.float32, device=dev) if by_user else None
+        nat.call("cmf_gen_fill", seed, m, n, f, thr_cell, thr_test, scale, int(by_user), lo, hi, nat.ptr(X),
+                 nat.ptr(T), nat.ptr(ptr), nat.ptr(minor), nat.ptr(val), nat.ptr(tptr), nat.ptr(tu), nat.ptr(tv),
+                 nat.ptr(tr), st)
+        return (ptr, minor, val), (Triples(tu, tv, tr) if by_user else None)
+
+    x_view, test = side(True, u0, u1)
+    t_view, _ = side(False, v0, v1)
+    return StreamShard(m, n, (u0, u1), (v0, v1), x_view, t_view, test, X, T)
+
+
+def gen_synthetic_stream(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1, test_fraction: float = 0.1,
+                         seed: int = 0):
+    """The whole matrix from the streaming generator: (DeviceRatings, test Triples)."""
+    sh = gen_stream_shard(m, n, f, nnz, noise_sigma, test_fraction, seed)
+    (rp, ci, cv), (cp, ri, rv) = sh.x_view, sh.t_view
+    return DeviceRatings(m, n, int(ci.numel()), rp, ci, cv, cp, ri, rv), sh.test
+
+
 def gen_synthetic_device(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1,
                          test_fraction: float = 0.1, seed: int = 0, row_chunk: int | None = None):
     """Fast on-GPU generator for benchmark shapes (Netflix / Yahoo / Hugewiki).
