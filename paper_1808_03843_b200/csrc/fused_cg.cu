@@ -68,7 +68,9 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
     unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     const int f = g.f;
     const int64_t P = packed_size(f);
-    const int SB = static_cast<int>((P * 2 + 127) & ~127ll);  // staging bytes per system
+    // staging bytes per system: every packed index a KP-wide expansion can touch
+    // (j(j+1)/2 + i for j < KP, i < 128), the part past P zero (columns j >= f)
+    constexpr int SB = (((KP * (KP - 1) / 2 + 128) * 2) + 127) & ~127;
     // per-group scratch: the matvec operand must sit on a 1024-byte swizzle atom
     const int GS = (MVB_BYTES + 2 * SB + 1023) & ~1023;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = warp >> 2;
@@ -119,29 +121,56 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
         float xi = act ? g.x0[sys * f + i] : 0.0f;
         const float bi = act ? g.b[sys * f + i] : 0.0f;
         cp_async_wait<1>();
+        if (gt == (nchunk - 1) % 128)  // the last 16-byte chunk may carry stride padding past P
+            for (int k = static_cast<int>(P); k < 8 * nchunk; ++k)
+                reinterpret_cast<unsigned short *>(stg + buf * SB)[k] = 0;
         named_bar(1 + grp, CG_THREADS);
         // row i of the symmetric matrix -> binary16 pairs in TMEM
         const __half *A = reinterpret_cast<const __half *>(stg + buf * SB);
         // element (i, j): row i of the packed lower triangle for j <= i, column i
-        // (row j, position i) above the diagonal; j is warp-uniform, so the
-        // column reads of a warp are consecutive halves.  32-bit offsets; lanes
-        // i >= f read element 0 (their rows only feed their own, unused outputs)
+        // (row j, position i) above the diagonal.  Warp q holds rows 32q .. 32q+31,
+        // so a 32-column chunk c is, for the whole warp, either below the diagonal
+        // (c < q: a contiguous segment of row i, read as realigned 32-bit words),
+        // above it (c > q: column i of rows j -- consecutive lanes read consecutive
+        // halves, offsets j(j+1)/2 are immediates) or the diagonal chunk (per
+        // element select).  Columns j >= f read the zero tail of the staging
+        // buffer; lanes i >= f read row 0 (their rows only feed their own, unused
+        // outputs).
         const int ri = act ? i * (i + 1) / 2 : 0;
         const int ci = act ? i : 0;
+        const int wq = warp & 3;
         const unsigned short *Au = reinterpret_cast<const unsigned short *>(A);
+        const uint32_t *Aw = reinterpret_cast<const uint32_t *>(A);
+        const uint32_t sel = (ri & 1) ? 0x5432u : 0x3210u;
 #pragma unroll
         for (int c = 0; c < (KP + 31) / 32; ++c) {  // fully unrolled: j, j(j+1)/2 are immediates
             uint32_t h[16];
+            if (c < wq) {
+                const int wb = (ri + 32 * c) >> 1;
+                uint32_t wv[17];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                uint32_t e[2];
+                for (int k = 0; k < 17; ++k) wv[k] = Aw[wb + k];
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    const int j = 32 * c + 2 * q + t;
-                    e[t] = 0u;
-                    if (j < f) e[t] = Au[j <= ci ? ri + j : j * (j + 1) / 2 + ci];
+                for (int q = 0; q < 16; ++q) h[q] = __byte_perm(wv[q], wv[q + 1], sel);
+            } else if (c > wq) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int j = 32 * c + 2 * q;
+                    if (j >= KP) break;
+                    h[q] = static_cast<uint32_t>(Au[j * (j + 1) / 2 + ci]) |
+                           (static_cast<uint32_t>(Au[(j + 1) * (j + 2) / 2 + ci]) << 16);
                 }
-                h[q] = e[0] | (e[1] << 16);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    uint32_t e[2];
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const int j = 32 * c + 2 * q + t;
+                        e[t] = j < KP ? Au[j <= ci ? ri + j : j * (j + 1) / 2 + ci] : 0u;
+                    }
+                    h[q] = e[0] | (e[1] << 16);
+                }
             }
             if (16 * c + 16 <= KP / 2) tmem_st16(slot_t + 16 * c, h);
             else if (16 * c < KP / 2) tmem_st8(slot_t + 16 * c, h);
@@ -283,7 +312,8 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
 template <int KP>
 static int launch_cg_tc(const tc::CgTcArgs &g, cudaStream_t st) {
     const int64_t P = packed_size(g.f);
-    const size_t SB = (P * 2 + 127) & ~127ll;
+    (void)P;
+    constexpr size_t SB = (((KP * (KP - 1) / 2 + 128) * 2) + 127) & ~127;  // as in cg_tc_kernel
     const size_t GS = (tc::MVB_BYTES + 2 * SB + 1023) & ~static_cast<size_t>(1023);
     const size_t smem = 1024 + tc::CGT_GROUPS * GS + tc::CGT_GROUPS * 8 + 16;
     auto k = tc::cg_tc_kernel<KP>;
