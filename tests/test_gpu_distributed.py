@@ -27,10 +27,22 @@ def _free_port():
 
 def _run(rank, world, solver, peer=False, per_rank=False):
     import paper_1808_03843_b200 as cmfb
-    from paper_1808_03843_b200.distributed import ShardedALS, shard_ratings
+    from paper_1808_03843_b200.distributed import ShardedALS, ShardedRatings, shard_ratings
     torch.cuda.set_device(0)
     m, n, nnz = SHAPE
-    if per_rank:
+    if per_rank == "stream":
+        # the streaming generator: each rank generates only its CSR rows / CSC columns
+        ub = [s * m // world for s in range(world + 1)]
+        vb = [s * n // world for s in range(world + 1)]
+        sh = cmfb.gen_stream_shard(m, n, F, nnz, 0.1, 0.1, 3, users=(ub[rank], ub[rank + 1]),
+                                   items=(vb[rank], vb[rank + 1]))
+        if world == 1:
+            train = cmfb.DeviceRatings(m, n, int(sh.x_view[1].numel()), *sh.x_view, *sh.t_view)
+        else:
+            tot = torch.tensor([sh.x_view[1].numel()], dtype=torch.int64)
+            dist.all_reduce(tot)
+            train = ShardedRatings(m, n, int(tot.item()), ub, vb, sh.x_view, sh.t_view)
+    elif per_rank:
         # reference protocol on the host, each rank builds only its shards
         t, _ = cmfb.gen_synthetic(m, n, F, nnz / (m * n), 0.1, 3)
         train = shard_ratings(t, m, n, rank, world)
@@ -66,12 +78,14 @@ def _worker(rank, world, port, out, solver, peer=False, per_rank=False):
 
 
 @pytest.mark.parametrize("solver,peer,per_rank", [("cg16", False, False), ("exact", False, False),
-                                                  ("cg16", True, False), ("cg16", True, True)])
+                                                  ("cg16", True, False), ("cg16", True, True),
+                                                  ("cg16", True, "stream"), ("exact", False, "stream")])
 def test_two_rank_engine_equals_single_rank(tmp_path, solver, peer, per_rank):
     """peer=True: the fused kernel stores each solved row into the other rank's
     replica through a CUDA-IPC mapping (cmf_fused_cg_update_peers) instead of
     an all-gather.  per_rank=True: each rank builds only its own shards from the
-    host triples (distributed.shard_ratings)."""
+    host triples (distributed.shard_ratings); "stream": each rank generates only
+    its own shards (gen_stream_shard, row-balanced ranges)."""
     out = str(tmp_path / "r")
     mp.spawn(_worker, args=(2, _free_port(), out, solver, peer, per_rank), nprocs=2, join=True)
     x1, th1, _ = _run(0, 1, solver, per_rank=per_rank)
