@@ -9,20 +9,22 @@
 // exactly the register-resident row layout the CG matvec wants (thread i <->
 // TMEM lane i <-> row i of A_u), so the solve runs straight out of TMEM:
 //
-//   warps 12-18 producers  cp.async gather of binary16 factor rows (+ the rating
-//                          rows) into a 12-stage swizzled operand ring
-//   warp 19     MMA        tcgen05.mma kind::f16 chain per row into TMEM buffer
-//                          (row % 3); tcgen05.commit -> stage empty / tmem full
-//   warps 0-11  CG         three groups of 4 warps, one per TMEM buffer: read
-//                          b_u from the accumulator's rating columns, repack
-//                          A_u to binary16 in place (the tcgen05 A-operand
-//                          layout), run Algorithm 1 (PAPER.md:272-293,
-//                          corrected r -= alpha*A p) in its pipelined form (one
-//                          barrier per iteration carries both dot products and
-//                          the next matvec's vector) with fp32 vectors; every
-//                          matvec is 7 tensor-core MMAs with A read from TMEM;
-//                          deterministic reductions; write x_u in place (warm
-//                          start = previous x_u), then free the buffer.
+//   producers   cp.async gather of binary16 factor rows (+ the rating rows)
+//               into a 12-stage swizzled operand ring (7 warps; 11 for long rows)
+//   MMA warp    tcgen05.mma kind::f16 chain per row into one of 2 (3) fp32 TMEM
+//               accumulators; tcgen05.commit -> stage empty / accumulator full
+//   CG groups   4 (2 for long rows) groups of 4 warps; group r % NG takes row r:
+//               reads b_u from the accumulator's rating columns, repacks A_u to
+//               binary16 into its own TMEM slot (the tcgen05 A-operand layout)
+//               and frees the accumulator, then runs Algorithm 1 (PAPER.md:
+//               272-293, corrected r -= alpha*A p) in its pipelined form (one
+//               barrier per iteration carries both dot products and the next
+//               matvec's vector) with fp32 vectors; every matvec is 7
+//               tensor-core MMAs with A read from TMEM; deterministic
+//               reductions; x_u written in place (warm start = previous x_u).
+// The kernel template lives in fused_cg.cuh (shared with the implicit-feedback
+// instances, fused_implicit.cu); this file holds the launchers, the two-pass
+// driver for long rows and the two-step route's batched CG (cg_tc_kernel).
 //
 // Semantics vs the reference: the diagonal gets lambda*n_u (weighted) or
 // lambda; rows with n_u == 0 are left untouched; eps = cg_tol * ||b_u||;

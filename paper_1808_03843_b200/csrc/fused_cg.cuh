@@ -662,11 +662,7 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
             int bd = 0, nit = 0;
             cg.tr = (ga.trace && r_here < 64) ? ga.trace + 40960 + 64 * r_here : nullptr;
             cg.trk = 0;
-#ifdef CMF_WEIGHTED_PIPELINED
-            if constexpr (false)
-#else
             if constexpr (WEIGHTED)  // ill-conditioned implicit systems: the standard recurrence
-#endif
                 cg.solve_standard(a_tmem, dcol, bi, -1.0, g.tol, g.f_s, xi, bd, nit, reg);
             else
                 cg.solve(a_tmem, dcol, reg, bi, -1.0, g.tol, g.f_s, xi, bd, nit);

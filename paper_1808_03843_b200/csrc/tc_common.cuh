@@ -63,15 +63,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
 // waiting for long rows use a longer cap so idle warps stay off the issue slots).
 template <uint32_t NS0 = 32, uint32_t NSMAX = 512>
 __device__ __forceinline__ void mbar_wait_backoff(uint32_t a, uint32_t parity) {
-#if defined(CMF_SUSPEND_ALL)
-    mbar_wait(a, parity);
-    return;
-#elif defined(CMF_SUSPEND_PROD)
-    if (NSMAX <= 512) {
-        mbar_wait(a, parity);
-        return;
-    }
-#endif
     uint32_t ok = 0, ns = NS0;
     while (true) {
         asm volatile(
