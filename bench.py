@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--no-ttr", action="store_true", help="skip time-to-RMSE")
     ap.add_argument("--no-next", action="store_true",
                     help="skip the SURVEY 8(f) rows (implicit iteration, eval, build)")
+    ap.add_argument("--exchange", default="replicate", choices=["replicate", "rs"],
+                    help="N > 1 with --data stream: 'rs' keeps X sharded and reduce-scatters partial item "
+                         "Grams (distributed.ReduceScatterALS) instead of replicating X")
     ap.add_argument("--data", default=None, choices=["reference", "device", "stream"],
                     help="reference: the reference's host generator + split (bit-identical "
                          "inputs; default for netflix / ml1m); device: the fast on-GPU generator")
@@ -343,19 +346,23 @@ def main():
         ub = [s * m // world for s in range(world + 1)]
         vb = [s * n // world for s in range(world + 1)]
         sh = cmfb.gen_stream_shard(m, n, f, nnz, 0.1, 0.1, 0, users=(ub[rank], ub[rank + 1]),
-                                   items=(vb[rank], vb[rank + 1]))
+                                   items=(vb[rank], vb[rank + 1]), local_csc=args.exchange == "rs")
         del sh.x_true, sh.t_true
         t_host = 0.0
         test = sh.test
         local_nnz = int(sh.x_view[1].numel())
-        if world == 1:
+        if args.exchange == "rs":
+            rs_shard = sh
+            shards = None
+        elif world == 1:
             shards = cmfb.DeviceRatings(m, n, local_nnz, *sh.x_view, *sh.t_view)
         else:
             tot = torch.tensor([local_nnz], dtype=torch.int64,
                                device="cuda" if dist.get_backend() == "nccl" else "cpu")
             dist.all_reduce(tot)
             shards = cdist.ShardedRatings(m, n, int(tot.item()), ub, vb, sh.x_view, sh.t_view)
-        del sh
+        if args.exchange != "rs":
+            del sh
         data_desc = ("synthetic, streaming generator (gen.cu): counter-based Bernoulli cells, U[-0.5,0.5) "
                      "rank-f truth, Irwin-Hall noise sigma 0.1, 10% holdout; each rank generates only its "
                      "CSR rows and CSC columns on its GPU (row-balanced ranges)")
@@ -375,7 +382,7 @@ def main():
                      "uniform cells, 10% holdout; not the reference's draw sequence)")
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
-    total_nnz = shards.nnz
+    total_nnz = shards.nnz if shards is not None else 0
     if world == 1 and fixture is not None:
         # the inputs are the fixture's inputs, byte for byte
         inputs["csr_digest_match"] = digest(*(a.cpu().numpy() for a in (
@@ -385,8 +392,17 @@ def main():
     x0 = torch.from_numpy(cmfb.init_factors(m, f, 0.1, [0, 0])).cuda()
     th0 = torch.from_numpy(cmfb.init_factors(n, f, 0.1, [0, 1])).cuda()
 
-    engine = cdist.ShardedALS(shards, f, lam=0.05, solver=solver, gram_kernel=args.gram_kernel,
-                              rank=rank, world=world)
+    if args.exchange == "rs":
+        if data_kind != "stream":
+            raise SystemExit("--exchange rs needs --data stream")
+        engine = cdist.ReduceScatterALS(rs_shard, f, lam=0.05, solver=solver, rank=rank, world=world)
+        x0 = x0[engine.u0:engine.u1].contiguous()  # X stays sharded
+        test = cmfb.Triples(test.user - engine.u0, test.item, test.rating)
+        total_nnz = engine.n_global
+        del rs_shard, sh
+    else:
+        engine = cdist.ShardedALS(shards, f, lam=0.05, solver=solver, gram_kernel=args.gram_kernel,
+                                  rank=rank, world=world)
 
     def run_steps(x, th, k, record=None):
         for _ in range(k):
@@ -395,7 +411,10 @@ def main():
     # ---- warm-up, then the timed region (K iterations, events on the launch stream)
     x, th = x0.clone(), th0.clone()
     exchange = "none (single GPU)" if world == 1 else "NCCL all-gather after each half"
-    if world > 1 and os.environ.get("CMF_PEER_STORE", "1") != "0":
+    if args.exchange == "rs":
+        exchange = ("reduce-scatter of partial item Grams (X sharded, no replica) + Theta all-gather"
+                    if world > 1 else "reduce-scatter route on one rank (pass 1 -> partial -> pass 2)")
+    elif world > 1 and os.environ.get("CMF_PEER_STORE", "1") != "0":
         # the fused kernel stores solved rows into every rank's replica (CUDA IPC
         # over NVLink) instead of an all-gather; any setup failure keeps NCCL
         try:

@@ -184,6 +184,26 @@ int cmf_fused_cg_update_implicit(const int64_t *indptr, const int32_t *indices, 
 int64_t cmf_fused_cg_workspace_bytes(int64_t nrows, int32_t f);
 /* Row stride (floats) of cmf_fused_cg_update_implicit's gram_full; -1 if f > 120. */
 int32_t cmf_fused_base_ld(int32_t f);
+/*
+ * One pass of the fused kernel's two-pass scheme with a caller-owned segment
+ * split and partial-accumulator buffer (the multi-GPU reduce-scatter exchange
+ * for tall-skinny data):
+ *   pass 1: gathers positions [indptr[u], seg[u]) of each row and stores the
+ *           fp32 accumulator (Gram + the two bias columns) of row u at
+ *           partial + (u*f + i) * pws, i < f, pws = roundup4(cmf_tc_width(f) + 2);
+ *           nothing is solved.  Rows without ratings store nothing (zero the
+ *           buffer first when it is summed across ranks).
+ *   pass 2: gathers [seg[u], indptr[u+1]), adds the row's partial, adds
+ *           lam*n_u (n_u = indptr[u+1] - indptr[u]) and solves into target.
+ *           With seg[u] == indptr[u+1] the row is solved from the partial alone.
+ * cmf_fused_cg_partial_floats(nrows, f) = floats of the partial buffer.  f <= 104.
+ */
+int cmf_fused_cg_pass(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
+                      int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
+                      int32_t weighted_reg, float *target, float *const *peer_targets, int32_t npeers,
+                      const int64_t *seg, float *partial, int32_t pass, int32_t f_s, double cg_tol,
+                      int32_t *breakdowns, int32_t *overflow_flag, void *stream);
+int64_t cmf_fused_cg_partial_floats(int64_t nrows, int32_t f);
 /* CUDA IPC for the peer replicas: export a device pointer (any address inside
  * an allocation) as a 64-byte handle + offset; open it in another process
  * (peer access enabled lazily over NVLink); close with the same offset. */
@@ -361,14 +381,19 @@ int cmf_mpr_count(const int64_t *pos_ptr, const int32_t *pos_item, int64_t m, co
  *                   user, item; float32 rating) of those users at tptr.
  * by_user = 1 gives a CSR shard, 0 a CSC shard; concatenated shards equal
  * data.build of the generated triples byte for byte (tests/test_gpu_gen.py).
+ * Minors (items for a CSR shard, users for a CSC shard) are restricted to
+ * [minor_lo, minor_hi) and written relative to minor_lo (a rank's local CSC
+ * over its own users for the reduce-scatter exchange); the full range gives
+ * global ids.
  */
 int cmf_gen_truth(uint64_t seed, int32_t which, int64_t rows, int32_t f, float *out, void *stream);
 int cmf_gen_count(uint64_t seed, int64_t m, int64_t n, uint64_t thr_cell, uint64_t thr_test, int32_t by_user,
-                  int64_t lo, int64_t hi, int64_t *ptr, int64_t *tptr, int64_t *scratch, void *stream);
+                  int64_t lo, int64_t hi, int64_t minor_lo, int64_t minor_hi, int64_t *ptr, int64_t *tptr,
+                  int64_t *scratch, void *stream);
 int cmf_gen_fill(uint64_t seed, int64_t m, int64_t n, int32_t f, uint64_t thr_cell, uint64_t thr_test,
-                 float noise_scale, int32_t by_user, int64_t lo, int64_t hi, const float *X, const float *T,
-                 const int64_t *ptr, int32_t *minor_out, float *val_out, const int64_t *tptr, int64_t *test_u,
-                 int64_t *test_v, float *test_r, void *stream);
+                 float noise_scale, int32_t by_user, int64_t lo, int64_t hi, int64_t minor_lo, int64_t minor_hi,
+                 const float *X, const float *T, const int64_t *ptr, int32_t *minor_out, float *val_out,
+                 const int64_t *tptr, int64_t *test_u, int64_t *test_v, float *test_r, void *stream);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,9 @@ _SIGNATURES = {
                                               _vp, _vp, _i32, _i32, _f64, _vp, _vp, _vp, _i64, _vp]),
     "cmf_fused_cg_workspace_bytes": (ctypes.c_int64, [_i64, _i32]),
     "cmf_fused_base_ld": (ctypes.c_int32, [_i32]),
+    "cmf_fused_cg_pass": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _i32, _vp, _vp, _i32,
+                                         _vp, _vp, _i32, _i32, _f64, _vp, _vp, _vp]),
+    "cmf_fused_cg_partial_floats": (ctypes.c_int64, [_i64, _i32]),
     "cmf_fused_cg_update_implicit": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _f64, _f64,
                                                     _vp, _vp, _vp, _i32, _i32, _f64, _vp, _vp, _vp, _i64, _vp]),
     "cmf_factors_to_half": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp]),
@@ -79,10 +82,10 @@ _SIGNATURES = {
     "cmf_mpr_count": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp]),
     "cmf_gen_truth": (ctypes.c_int, [ctypes.c_uint64, _i32, _i64, _i32, _vp, _vp]),
     "cmf_gen_count": (ctypes.c_int, [ctypes.c_uint64, _i64, _i64, ctypes.c_uint64, ctypes.c_uint64, _i32, _i64,
-                                     _i64, _vp, _vp, _vp, _vp]),
+                                     _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "cmf_gen_fill": (ctypes.c_int, [ctypes.c_uint64, _i64, _i64, _i32, ctypes.c_uint64, ctypes.c_uint64,
-                                    ctypes.c_float, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                                    _vp]),
+                                    ctypes.c_float, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _vp, _vp]),
 }
 EXPORTED = tuple(_SIGNATURES)
 REDUCE_SLOTS = 1024  # eval.cu: doubles an eval `out` buffer must hold
@@ -137,7 +140,7 @@ def check(rc: int, what: str = ""):
 
 # Kernel-launching entry points called since the counter was last reset (the
 # benchmark's "gpu_launches" claim counts launches of OUR kernels).
-_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_fused_cg_update_ws": 1, "cmf_fused_cg_update_implicit": 1, "cmf_dense_gram": 2, "cmf_implicit_loss_csr": 2, "cmf_group_rows": 6, "cmf_mpr_count": 1, "cmf_gen_truth": 1, "cmf_gen_count": 3, "cmf_gen_fill": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
+_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_fused_cg_update_ws": 1, "cmf_fused_cg_update_implicit": 1, "cmf_fused_cg_pass": 1, "cmf_dense_gram": 2, "cmf_implicit_loss_csr": 2, "cmf_group_rows": 6, "cmf_mpr_count": 1, "cmf_gen_truth": 1, "cmf_gen_count": 3, "cmf_gen_fill": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
                 "cmf_batch_cholesky": 1, "cmf_pack_half": 1, "cmf_sq_error": 2,
                 "cmf_sq_error_csr": 2, "cmf_weighted_sqnorm": 2, "cmf_predict_pairs": 1}
 LAUNCHES = [0]

@@ -28,7 +28,8 @@ int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, in
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
                     int, float *, float *const *, int, int64_t, int, double, int32_t *, int32_t *, void *, int64_t,
-                    const float *, float, bool, cudaStream_t);
+                    const float *, float, bool, const int64_t *, float *, int, cudaStream_t);
+int64_t fused_cg_partial_floats(int64_t nrows, int f);
 int64_t fused_cg_workspace_bytes(int64_t nrows, int W);
 int factors_to_half_launch(const float *, int64_t, int, void *, int, int32_t *, cudaStream_t);
 int spmm_bias_launch(const int64_t *, const int32_t *, const float *, int64_t, const float *, int,
@@ -51,11 +52,11 @@ int build_launch(const void *, const void *, bool, const float *, int64_t, int64
 int64_t build_workspace_bytes(int64_t k);
 int fused_base_ld(int f);
 int gen_truth_launch(uint64_t, int, int64_t, int, float *, cudaStream_t);
-int gen_count_launch(uint64_t, int64_t, int64_t, uint64_t, uint64_t, int, int64_t, int64_t, int64_t *, int64_t *,
-                     int64_t *, cudaStream_t);
-int gen_fill_launch(uint64_t, int64_t, int64_t, int, uint64_t, uint64_t, float, int, int64_t, int64_t, const float *,
-                    const float *, const int64_t *, int32_t *, float *, const int64_t *, int64_t *, int64_t *, float *,
-                    cudaStream_t);
+int gen_count_launch(uint64_t, int64_t, int64_t, uint64_t, uint64_t, int, int64_t, int64_t, int64_t, int64_t,
+                     int64_t *, int64_t *, int64_t *, cudaStream_t);
+int gen_fill_launch(uint64_t, int64_t, int64_t, int, uint64_t, uint64_t, float, int, int64_t, int64_t, int64_t,
+                    int64_t, const float *, const float *, const int64_t *, int32_t *, float *, const int64_t *,
+                    int64_t *, int64_t *, float *, cudaStream_t);
 int64_t group_workspace_bytes(int64_t k);
 int group_launch(const void *, const void *, bool, int64_t, int64_t, int64_t *, int32_t *, void *, int64_t,
                  cudaStream_t);
@@ -223,7 +224,7 @@ int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const flo
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target, nullptr,
                            0, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, nullptr, 0.0f, false,
-                           S(stream));
+                           nullptr, nullptr, 0, S(stream));
 }
 
 int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, const float *values,
@@ -241,7 +242,7 @@ int cmf_fused_cg_update_peers(const int64_t *indptr, const int32_t *indices, con
     REQUIRE(ncols >= 1, "ncols must be >= 1");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
                            peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, nullptr, 0.0f,
-                           false, S(stream));
+                           false, nullptr, nullptr, 0, S(stream));
 }
 
 int cmf_fused_cg_update_ws(const int64_t *indptr, const int32_t *indices, const float *values,
@@ -262,7 +263,7 @@ int cmf_fused_cg_update_ws(const int64_t *indptr, const int32_t *indices, const 
     REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 255) == 0, "workspace must be 256-byte aligned");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
                            peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, workspace,
-                           workspace_bytes, nullptr, 0.0f, false, S(stream));
+                           workspace_bytes, nullptr, 0.0f, false, nullptr, nullptr, 0, S(stream));
 }
 
 int cmf_fused_cg_update_implicit(const int64_t *indptr, const int32_t *indices, const float *values,
@@ -284,7 +285,30 @@ int cmf_fused_cg_update_implicit(const int64_t *indptr, const int32_t *indices, 
     REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 255) == 0, "workspace must be 256-byte aligned");
     return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, 0, target, peer_targets,
                            npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, workspace, workspace_bytes, gram_full,
-                           static_cast<float>(alpha), true, S(stream));
+                           static_cast<float>(alpha), true, nullptr, nullptr, 0, S(stream));
+}
+
+int cmf_fused_cg_pass(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
+                      int64_t nnz, const void *fixed16, int64_t ncols, int32_t w16, int32_t f, double lam,
+                      int32_t weighted_reg, float *target, float *const *peer_targets, int32_t npeers,
+                      const int64_t *seg, float *partial, int32_t pass, int32_t f_s, double cg_tol,
+                      int32_t *breakdowns, int32_t *overflow_flag, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1, "bad dimensions");
+    REQUIRE(pass == 1 || pass == 2, "pass must be 1 or 2");
+    REQUIRE(f_s >= 1, "cg_iters must be >= 1");
+    REQUIRE(cg_tol >= 0.0, "cg_tol must be >= 0");
+    REQUIRE(npeers >= 0 && npeers <= 64, "npeers must be in [0, 64]");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && fixed16 && target && seg && partial, "null argument");
+    REQUIRE(npeers == 0 || peer_targets, "null peer list");
+    REQUIRE(ncols >= 1, "ncols must be >= 1");
+    return fused_cg_launch(indptr, indices, values, nrows, fixed16, ncols, w16, f, lam, weighted_reg, target,
+                           peer_targets, npeers, nnz, f_s, cg_tol, breakdowns, overflow_flag, nullptr, 0, nullptr,
+                           0.0f, false, seg, partial, pass, S(stream));
+}
+
+int64_t cmf_fused_cg_partial_floats(int64_t nrows, int32_t f) {
+    return (nrows < 0 || f < 1) ? -1 : fused_cg_partial_floats(nrows, f);
 }
 
 int32_t cmf_fused_base_ld(int32_t f) { return f < 1 ? -1 : fused_base_ld(f); }
@@ -424,23 +448,27 @@ int cmf_gen_truth(uint64_t seed, int32_t which, int64_t rows, int32_t f, float *
 }
 
 int cmf_gen_count(uint64_t seed, int64_t m, int64_t n, uint64_t thr_cell, uint64_t thr_test, int32_t by_user,
-                  int64_t lo, int64_t hi, int64_t *ptr, int64_t *tptr, int64_t *scratch, void *stream) {
+                  int64_t lo, int64_t hi, int64_t minor_lo, int64_t minor_hi, int64_t *ptr, int64_t *tptr,
+                  int64_t *scratch, void *stream) {
     REQUIRE(m >= 0 && n >= 0 && m < (int64_t(1) << 32) && n < (int64_t(1) << 31), "gen: bad extents");
     REQUIRE(lo >= 0 && hi >= lo && hi <= (by_user ? m : n), "gen: bad major range");
+    REQUIRE(minor_lo >= 0 && minor_hi >= minor_lo && minor_hi <= (by_user ? n : m), "gen: bad minor range");
     REQUIRE(ptr && (hi == lo || scratch), "null argument");
-    return gen_count_launch(seed, m, n, thr_cell, thr_test, by_user, lo, hi, ptr, tptr, scratch, S(stream));
+    return gen_count_launch(seed, m, n, thr_cell, thr_test, by_user, lo, hi, minor_lo, minor_hi, ptr, tptr, scratch,
+                            S(stream));
 }
 
 int cmf_gen_fill(uint64_t seed, int64_t m, int64_t n, int32_t f, uint64_t thr_cell, uint64_t thr_test,
-                 float noise_scale, int32_t by_user, int64_t lo, int64_t hi, const float *X, const float *T,
-                 const int64_t *ptr, int32_t *minor_out, float *val_out, const int64_t *tptr, int64_t *test_u,
-                 int64_t *test_v, float *test_r, void *stream) {
+                 float noise_scale, int32_t by_user, int64_t lo, int64_t hi, int64_t minor_lo, int64_t minor_hi,
+                 const float *X, const float *T, const int64_t *ptr, int32_t *minor_out, float *val_out,
+                 const int64_t *tptr, int64_t *test_u, int64_t *test_v, float *test_r, void *stream) {
     REQUIRE(m >= 0 && n >= 0 && m < (int64_t(1) << 32) && n < (int64_t(1) << 31) && f >= 1, "gen: bad extents");
     REQUIRE(lo >= 0 && hi >= lo && hi <= (by_user ? m : n), "gen: bad major range");
+    REQUIRE(minor_lo >= 0 && minor_hi >= minor_lo && minor_hi <= (by_user ? n : m), "gen: bad minor range");
     REQUIRE(X && T && ptr, "null argument");
     REQUIRE(!tptr || (by_user && test_u && test_v && test_r), "test triples come from the user pass");
-    return gen_fill_launch(seed, m, n, f, thr_cell, thr_test, noise_scale, by_user, lo, hi, X, T, ptr, minor_out,
-                           val_out, tptr, test_u, test_v, test_r, S(stream));
+    return gen_fill_launch(seed, m, n, f, thr_cell, thr_test, noise_scale, by_user, lo, hi, minor_lo, minor_hi, X, T,
+                           ptr, minor_out, val_out, tptr, test_u, test_v, test_r, S(stream));
 }
 
 int64_t cmf_group_workspace_bytes(int64_t k) { return k < 0 ? -1 : group_workspace_bytes(k); }

@@ -232,8 +232,9 @@ __global__ void segment_split_kernel(const int64_t *indptr, const int32_t *indic
 constexpr int64_t kTwoPassShadowBytes = int64_t(48) << 20;
 int64_t fused_cg_workspace_bytes(int64_t nrows, int W) {
     const int64_t pws = (W + 2 + 3) / 4 * 4;
-    return ((nrows * 8 + 255) & ~int64_t(255)) + nrows * 128 * pws * 4;
+    return ((nrows * 8 + 255) & ~int64_t(255)) + nrows * 128 * pws * 4;  // (f <= 128 lanes per row)
 }
+int64_t fused_cg_partial_floats(int64_t nrows, int f) { return nrows * f * ((gram_tc_width(f) + 2 + 3) / 4 * 4); }
 
 int fused_dispatch_implicit(tc::FusedArgs g, int f, bool long_rows, cudaStream_t st);
 
@@ -241,7 +242,7 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
                     const void *fixed16, int64_t ncols, int W, int f, double lam, int weighted, float *target,
                     float *const *peers, int npeers, int64_t nnz, int f_s, double cg_tol, int32_t *breakdowns,
                     int32_t *overflow, void *ws, int64_t ws_bytes, const float *base, float alpha, bool implicit,
-                    cudaStream_t st) {
+                    const int64_t *ext_seg, float *ext_partial, int ext_pass, cudaStream_t st) {
     if (nrows == 0) return CMF_OK;
     if (npeers < 0 || (npeers > 0 && peers == nullptr)) return set_error(CMF_EINVAL, "bad peer replica list");
     if (nnz < 0) return set_error(CMF_EINVAL, "negative rating count");
@@ -285,6 +286,17 @@ int fused_cg_launch(const int64_t *indptr, const int32_t *indices, const float *
     auto dispatch = [&](const tc::FusedArgs &a) {
         return implicit ? fused_dispatch_implicit(a, f, long_rows, st) : fused_dispatch_t<false>(a, f, long_rows, st);
     };
+    if (ext_pass == 1 || ext_pass == 2) {
+        // one pass of the two-pass scheme with the caller's segment split and
+        // partial buffer (multi-GPU reduce-scatter of partial Grams, distributed.py)
+        if (!ext_seg || !ext_partial) return set_error(CMF_EINVAL, "pass %d needs seg and partial", ext_pass);
+        if (f > 104) return set_error(CMF_EINVAL, "partial passes support f <= 104");
+        g.partial = ext_partial;
+        g.pws = (W + 2 + 3) / 4 * 4;
+        g.gather.seg = ext_seg;
+        g.gather.pass = ext_pass;
+        return dispatch(g);
+    }
     {
         const char *e = getenv("CMF_TWO_PASS");
         const bool want = e ? atoi(e) != 0

@@ -80,9 +80,10 @@ struct FusedArgs {
     int32_t *breakdowns;
     int32_t *overflow;  // set when a row's A_u does not fit binary16 (NumericalError)
     // Two-pass Gram (gather.pass 1 / 2, long rows over a fixed side larger than
-    // L2 can hold): pass 1 stores each row's partial accumulator (columns
-    // [0, W+2): the first-segment Gram and bias) at partial + (u*128 + i)*PWS
-    // for lanes i < f; pass 2 adds it to the second segment's accumulator.
+    // L2 can hold, or a multi-GPU reduce-scatter of partial Grams): pass 1 stores
+    // each row's partial accumulator (columns [0, W+2): the first-segment Gram
+    // and bias) at partial + (u*f + i)*PWS for lanes i < f; pass 2 adds it to the
+    // second segment's accumulator.
     float *partial;
     int pws;  // partial row stride in floats (roundup4(W + 2))
     // Implicit feedback (WEIGHTED kernels, implicit.py:57-84): A_u = base +
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
             if (i == 0 && r_here < 2048) trace_at(ga.trace, 32768 + 4 * r_here + 0);
             // long rows keep the group idle: back-off wait
             if (ga.pass == 2 && act) {  // the first segment's partial: into L2 while the Gram builds
-                const char *pr = reinterpret_cast<const char *>(g.partial + (u * 128 + i) * g.pws);
+                const char *pr = reinterpret_cast<const char *>(g.partial + (u * f + i) * g.pws);
                 for (int o = 0; o < g.pws * 4; o += 128)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(pr + o));
             }
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(FusedShape<FC, LONG>::THREADS, 1)
                 seg_acc = ga.pass == 1 ? sp > p0 : ga.indptr[u + 1] > sp;
                 seg_part = ga.pass == 2 && sp > p0;
             }
-            float *const prow = g.partial + (u * 128 + i) * g.pws;
+            float *const prow = g.partial + (u * f + i) * g.pws;
             if (ga.pass == 1) {
                 // first segment: park the fp32 accumulator (Gram + bias columns) in HBM
                 if (seg_acc) {

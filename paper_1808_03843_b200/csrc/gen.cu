@@ -65,13 +65,16 @@ __device__ __forceinline__ float rating(const Params &p, const float *xu, const 
 }
 
 // by_user: majors = users [lo, hi) (CSR), minors = items; else majors = items (CSC)
-__global__ void count_kernel(Params p, bool by_user, int64_t lo, int64_t hi, int64_t *cnt_train, int64_t *cnt_test) {
+// minors restricted to [mlo, mhi) (e.g. a rank's own users for the local CSC of
+// the reduce-scatter exchange); minor ids are written relative to mlo
+__global__ void count_kernel(Params p, bool by_user, int64_t lo, int64_t hi, int64_t mlo, int64_t mhi,
+                             int64_t *cnt_train, int64_t *cnt_test) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    const int64_t minors = by_user ? p.n : p.m;
+    const int64_t minors = mhi;
     for (int64_t r = lo + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); r < hi; r += warps) {
         int64_t ctr = 0, cte = 0;
-        for (int64_t c0 = 0; c0 < minors; c0 += 32) {
+        for (int64_t c0 = mlo; c0 < minors; c0 += 32) {
             const int64_t c = c0 + lane;
             bool in = false, te = false;
             if (c < minors) {
@@ -91,16 +94,16 @@ __global__ void count_kernel(Params p, bool by_user, int64_t lo, int64_t hi, int
 
 // fill: train cells of major r at ptr[r - lo] .. (minor ids ascending), test
 // cells (CSR pass only) at tptr[r - lo] .. as (user, item, rating) triples
-__global__ void fill_kernel(Params p, bool by_user, int64_t lo, int64_t hi, const float *X, const float *T,
-                            const int64_t *ptr, int32_t *minor_out, float *val_out, const int64_t *tptr,
-                            int64_t *tu, int64_t *tv, float *tr) {
+__global__ void fill_kernel(Params p, bool by_user, int64_t lo, int64_t hi, int64_t mlo, int64_t mhi,
+                            const float *X, const float *T, const int64_t *ptr, int32_t *minor_out, float *val_out,
+                            const int64_t *tptr, int64_t *tu, int64_t *tv, float *tr) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    const int64_t minors = by_user ? p.n : p.m;
+    const int64_t minors = mhi;
     const uint32_t below = (1u << lane) - 1u;
     for (int64_t r = lo + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); r < hi; r += warps) {
         int64_t pos = ptr[r - lo], tpos = tptr ? tptr[r - lo] : 0;
-        for (int64_t c0 = 0; c0 < minors; c0 += 32) {
+        for (int64_t c0 = mlo; c0 < minors; c0 += 32) {
             const int64_t c = c0 + lane;
             bool in = false, te = false;
             const uint64_t u = by_user ? r : c, v = by_user ? c : r;
@@ -114,7 +117,7 @@ __global__ void fill_kernel(Params p, bool by_user, int64_t lo, int64_t hi, cons
                 const float rv = rating(p, X + u * p.f, T + v * p.f, u, v);
                 if (!te) {
                     const int64_t q = pos + __popc(mtr & below);
-                    minor_out[q] = static_cast<int32_t>(c);
+                    minor_out[q] = static_cast<int32_t>(c - mlo);
                     val_out[q] = rv;
                 } else if (tptr) {
                     const int64_t q = tpos + __popc(mte & below);
@@ -194,7 +197,8 @@ int gen_truth_launch(uint64_t seed, int which, int64_t rows, int f, float *out, 
 }
 
 int gen_count_launch(uint64_t seed, int64_t m, int64_t n, uint64_t thr_cell, uint64_t thr_test, int by_user,
-                     int64_t lo, int64_t hi, int64_t *ptr, int64_t *tptr, int64_t *scratch, cudaStream_t st) {
+                     int64_t lo, int64_t hi, int64_t mlo, int64_t mhi, int64_t *ptr, int64_t *tptr, int64_t *scratch,
+                     cudaStream_t st) {
     const gen::Params p = make_params(seed, m, n, 1, thr_cell, thr_test, 0.0f);
     const int64_t nr = hi - lo;
     if (nr <= 0) {
@@ -203,20 +207,21 @@ int gen_count_launch(uint64_t seed, int64_t m, int64_t n, uint64_t thr_cell, uin
         return e == cudaSuccess ? CMF_OK : set_error(CMF_ECUDA, "gen: %s", cudaGetErrorString(e));
     }
     int64_t *cte = tptr ? scratch + nr : nullptr;
-    gen::count_kernel<<<grid_warps(nr), 256, 0, st>>>(p, by_user != 0, lo, hi, scratch, cte);
+    gen::count_kernel<<<grid_warps(nr), 256, 0, st>>>(p, by_user != 0, lo, hi, mlo, mhi, scratch, cte);
     gen::scan_i64_kernel<<<1, 1024, 0, st>>>(scratch, nr, ptr);
     if (tptr) gen::scan_i64_kernel<<<1, 1024, 0, st>>>(cte, nr, tptr);
     return check_launch("gen count");
 }
 
 int gen_fill_launch(uint64_t seed, int64_t m, int64_t n, int f, uint64_t thr_cell, uint64_t thr_test,
-                    float noise_scale, int by_user, int64_t lo, int64_t hi, const float *X, const float *T,
+                    float noise_scale, int by_user, int64_t lo, int64_t hi, int64_t mlo, int64_t mhi, const float *X,
+                    const float *T,
                     const int64_t *ptr, int32_t *minor_out, float *val_out, const int64_t *tptr, int64_t *tu,
                     int64_t *tv, float *tr, cudaStream_t st) {
     const gen::Params p = make_params(seed, m, n, f, thr_cell, thr_test, noise_scale);
     if (hi <= lo) return CMF_OK;
-    gen::fill_kernel<<<grid_warps(hi - lo), 256, 0, st>>>(p, by_user != 0, lo, hi, X, T, ptr, minor_out, val_out,
-                                                          tptr, tu, tv, tr);
+    gen::fill_kernel<<<grid_warps(hi - lo), 256, 0, st>>>(p, by_user != 0, lo, hi, mlo, mhi, X, T, ptr, minor_out,
+                                                          val_out, tptr, tu, tv, tr);
     return check_launch("gen fill");
 }
 

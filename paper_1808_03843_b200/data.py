@@ -406,7 +406,8 @@ class StreamShard:
 
 
 def gen_stream_shard(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1, test_fraction: float = 0.1,
-                     seed: int = 0, users: tuple | None = None, items: tuple | None = None) -> StreamShard:
+                     seed: int = 0, users: tuple | None = None, items: tuple | None = None,
+                     local_csc: bool = False) -> StreamShard:
     """Streaming synthetic generator (gen.cu): the CSR rows of
     users [u0, u1) and CSC rows of items [v0, v1) of a low-rank-plus-noise
     matrix with ~nnz train ratings, generated on the device in build() order
@@ -414,7 +415,10 @@ def gen_stream_shard(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1,
     another's shard, and the shards of all ranks tile the global matrix.  The
     model is gen_synthetic's (data.py:270-302: U[-1/2, 1/2) truth, uniformly
     random cells, dot + noise of variance sigma^2) but its draws are not the
-    reference's PCG64 stream (Bernoulli cells, Irwin-Hall noise)."""
+    reference's PCG64 stream (Bernoulli cells, Irwin-Hall noise).
+    ``local_csc``: the CSC covers ALL items but only this rank's users (ids
+    relative to u0) -- the input of the reduce-scatter exchange
+    (distributed.ReduceScatterALS) instead of the item range's CSC."""
     u0, u1 = users if users is not None else (0, m)
     v0, v1 = items if items is not None else (0, n)
     thr_cell, thr_test, scale = stream_params(m, n, nnz, noise_sigma, test_fraction)
@@ -425,12 +429,13 @@ def gen_stream_shard(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1,
     nat.call("cmf_gen_truth", seed, 0, m, f, nat.ptr(X), st)
     nat.call("cmf_gen_truth", seed, 1, n, f, nat.ptr(T), st)
 
-    def side(by_user, lo, hi):
+    def side(by_user, lo, hi, mlo=0, mhi=None):
+        mhi = (n if by_user else m) if mhi is None else mhi
         nr = hi - lo
         ptr = torch.empty(nr + 1, dtype=torch.int64, device=dev)
         tptr = torch.empty(nr + 1, dtype=torch.int64, device=dev) if by_user else None
         scratch = torch.empty(max(2 * nr, 1), dtype=torch.int64, device=dev)
-        nat.call("cmf_gen_count", seed, m, n, thr_cell, thr_test, int(by_user), lo, hi, nat.ptr(ptr),
+        nat.call("cmf_gen_count", seed, m, n, thr_cell, thr_test, int(by_user), lo, hi, mlo, mhi, nat.ptr(ptr),
                  nat.ptr(tptr), nat.ptr(scratch), st)
         ntr = int(ptr[-1].item())
         nte = int(tptr[-1].item()) if by_user else 0
@@ -439,13 +444,17 @@ def gen_stream_shard(m: int, n: int, f: int, nnz: int, noise_sigma: float = 0.1,
         tu = torch.empty(nte, dtype=torch.int64, device=dev) if by_user else None
         tv = torch.empty(nte, dtype=torch.int64, device=dev) if by_user else None
         tr = torch.empty(nte, dtype=torch.float32, device=dev) if by_user else None
-        nat.call("cmf_gen_fill", seed, m, n, f, thr_cell, thr_test, scale, int(by_user), lo, hi, nat.ptr(X),
-                 nat.ptr(T), nat.ptr(ptr), nat.ptr(minor), nat.ptr(val), nat.ptr(tptr), nat.ptr(tu), nat.ptr(tv),
-                 nat.ptr(tr), st)
+        nat.call("cmf_gen_fill", seed, m, n, f, thr_cell, thr_test, scale, int(by_user), lo, hi, mlo, mhi,
+                 nat.ptr(X), nat.ptr(T), nat.ptr(ptr), nat.ptr(minor), nat.ptr(val), nat.ptr(tptr), nat.ptr(tu),
+                 nat.ptr(tv), nat.ptr(tr), st)
         return (ptr, minor, val), (Triples(tu, tv, tr) if by_user else None)
 
     x_view, test = side(True, u0, u1)
-    t_view, _ = side(False, v0, v1)
+    if local_csc:
+        # every item's ratings from this rank's users only, user ids relative to u0
+        t_view, _ = side(False, 0, n, u0, u1)
+    else:
+        t_view, _ = side(False, v0, v1)
     return StreamShard(m, n, (u0, u1), (v0, v1), x_view, t_view, test, X, T)
 
 

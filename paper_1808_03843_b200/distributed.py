@@ -298,3 +298,120 @@ class ShardedALS:
         if fx[2] or ft[2]:
             raise DataError("singular system(s) during sharded training")
         return fx[1] + ft[1]
+
+
+class ReduceScatterALS:
+    """Tall-skinny multi-GPU ALS without an X replica (the "better
+    exchange for tall-skinny" row).  Rank r owns the user
+    rows [ub[r], ub[r+1]) -- its rows of X only -- and the item rows
+    [vb[r], vb[r+1]); Theta (n x f, small when m >> n) is replicated.  One
+    iteration:
+
+      update-X on my users (fused kernel, fixed = Theta)              no exchange
+      pass 1 over my LOCAL CSC (every item x my users): each item's partial
+        Gram + bias from my users, fp32, into a partial buffer (n x f x pws)
+      reduce-scatter (sum) of the partial buffers: my items' complete accumulators
+      pass 2 on my items from the partial alone (empty gather segment, lambda n_v
+        with the global n_v)                                          -> Theta rows
+      all-gather Theta
+
+    The wire carries (k-1)/k of the partial buffer (Hugewiki, k = 8: ~2 GB per
+    rank) instead of (k-1)/k of X (17.5 GB), and no rank holds X.  The partials
+    of different ranks are summed in rank order, so results match the replicated
+    route up to fp32 summation order (CG route: RMSE parity).  Inputs come from
+    data.gen_stream_shard(..., local_csc=True)."""
+
+    def __init__(self, shard, f: int, lam: float, solver, rank: int = 0, world: int = 1, group=None):
+        import torch.distributed as dist
+        if not (solver.method == "cg" and resolve_gram_kernel("auto", solver, f) == "tc"):
+            raise DataError("the reduce-scatter exchange runs the fused CG route (precision='fp16')")
+        self.f, self.lam, self.solver = f, lam, solver
+        self.gram_kernel = "tc"
+        self.rank, self.world, self.group = rank, world, group
+        self.m, self.n = shard.m, shard.n
+        self.u0, self.u1 = shard.users
+        self.x_view, self.c_view = shard.x_view, shard.t_view
+        dev = self.x_view[0].device
+        n = self.n
+        nc = (n + world - 1) // world
+        self.nc = nc
+        self.vb = [min(s * nc, n) for s in range(world + 1)]
+        self.v0, self.v1 = self.vb[rank], self.vb[rank + 1]
+        # global per-item counts -> pass-2 pointers of my items (empty segments)
+        cnt = torch.diff(self.c_view[0])
+        if world > 1:
+            cnt = cnt.clone()
+            if dist.get_backend(group) == "gloo":
+                h = cnt.cpu()
+                dist.all_reduce(h, group=group)
+                cnt = h.to(dev)
+            else:
+                dist.all_reduce(cnt, group=group)
+        self.n_global = int(cnt.sum().item())
+        mine = cnt[self.v0:self.v1]
+        self.ptr2 = torch.zeros(mine.numel() + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(mine, 0, out=self.ptr2[1:])
+        self.seg1 = self.c_view[0][1:].contiguous()  # pass 1: the whole local row
+        self.seg2 = self.ptr2[1:].contiguous()        # pass 2: nothing to gather
+        pf = int(nat.lib().cmf_fused_cg_partial_floats(1, f))  # floats per item
+        self.pf = pf
+        self.partial = torch.empty(world * nc * pf, dtype=torch.float32, device=dev)
+        self.mine = torch.empty(nc * pf, dtype=torch.float32, device=dev)
+        self.x_plan = HalfUpdatePlan(self.u1 - self.u0, f, solver, dev)
+        self.c_plan = HalfUpdatePlan(n, f, solver, dev)
+        self.t_gather = RowGather(self.vb, f, dev) if world > 1 else None
+
+    def local_rows(self):
+        return {"x": self.u1 - self.u0, "t": self.v1 - self.v0}
+
+    def local_nnz(self):
+        """Ratings this rank gathers per half: its users' CSR rows and its local CSC."""
+        return {"x": int(self.x_view[1].numel()), "t": int(self.c_view[1].numel())}
+
+    def attach_replicas(self, x, theta) -> bool:  # no X replica, no peer stores
+        return False
+
+    def detach_replicas(self):
+        pass
+
+    def _reduce_scatter(self):
+        import torch.distributed as dist
+        if self.world == 1:
+            self.mine.copy_(self.partial[: self.nc * self.pf])
+            return
+        if dist.get_backend(self.group) == "gloo":  # ranks sharing a device (tests): via host memory
+            h = self.partial.cpu()
+            dist.all_reduce(h, group=self.group)
+            self.mine.copy_(h[self.rank * self.nc * self.pf:(self.rank + 1) * self.nc * self.pf])
+            return
+        dist.reduce_scatter_tensor(self.mine, self.partial, group=self.group)
+
+    def iteration(self, x_local, theta, record=None):
+        """x_local: this rank's rows of X ((u1-u0) x f), theta: the full replica."""
+        s, f = self.solver, self.f
+        st = nat.stream_ptr()
+        xp, xi, xv = self.x_view
+        self.x_plan.launch(xp, xi, xv, theta, x_local, self.lam, True, "tc", record)
+        cp, ci, cv = self.c_view
+        shadow, _ = self.c_plan._shadow(x_local)
+        self.partial.zero_()
+        common = (nat.ptr(shadow), self.u1 - self.u0, self.c_plan.w16, f, float(self.lam), 1)
+        nat.call("cmf_fused_cg_pass", nat.ptr(cp), nat.ptr(ci), nat.ptr(cv), self.n, int(ci.numel()), *common,
+                 nat.ptr(theta), None, 0, nat.ptr(self.seg1), nat.ptr(self.partial), 1, int(s.cg_iters),
+                 float(s.cg_tol), nat.ptr(self.c_plan.flags) + 4, nat.ptr(self.c_plan.flags), st)
+        self._reduce_scatter()
+        nv = self.v1 - self.v0
+        if nv:
+            nat.call("cmf_fused_cg_pass", nat.ptr(self.ptr2), nat.ptr(ci), nat.ptr(cv), nv, 0, *common,
+                     nat.ptr(theta) + 4 * self.v0 * f, None, 0, nat.ptr(self.seg2), nat.ptr(self.mine), 2,
+                     int(s.cg_iters), float(s.cg_tol), nat.ptr(self.c_plan.flags) + 4, nat.ptr(self.c_plan.flags),
+                     st)
+        if self.t_gather is not None:
+            self.t_gather(theta, self.rank, self.group)
+
+    def check(self):
+        for plan in (self.x_plan, self.c_plan):
+            fl = plan.read_flags()
+            if fl[0]:
+                raise NumericalError("Gram entries overflow binary16 range (+-65504); "
+                                     "rescale the ratings before using half precision")

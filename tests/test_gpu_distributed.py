@@ -121,3 +121,68 @@ def test_per_rank_shards_concatenate_to_build(cuda_device):
             assert np.array_equal(np.concatenate([[0]] + ptrs), ref[0])
             assert np.array_equal(np.concatenate(idxs), ref[1])
             assert np.array_equal(np.concatenate(vals).view(np.uint32), ref[2].view(np.uint32))
+
+
+def _run_rs(rank, world):
+    """The reduce-scatter exchange (distributed.ReduceScatterALS) on streamed
+    shards: X stays sharded, partial item Grams are summed across ranks."""
+    import paper_1808_03843_b200 as cmfb
+    from paper_1808_03843_b200.distributed import ReduceScatterALS
+    torch.cuda.set_device(0)
+    m, n, nnz = SHAPE
+    ub = [s * m // world for s in range(world + 1)]
+    sh = cmfb.gen_stream_shard(m, n, F, nnz, 0.1, 0.1, 3, users=(ub[rank], ub[rank + 1]), local_csc=True)
+    eng = ReduceScatterALS(sh, F, lam=0.05, solver=cmfb.SolverConfig("cg", precision="fp16"), rank=rank,
+                           world=world)
+    x = torch.from_numpy(cmfb.init_factors(m, F, 0.1, [0, 0])).cuda()[ub[rank]:ub[rank + 1]].contiguous()
+    th = torch.from_numpy(cmfb.init_factors(n, F, 0.1, [0, 1])).cuda()
+    for _ in range(ITERS):
+        eng.iteration(x, th)
+    eng.check()
+    torch.cuda.synchronize()
+    te = sh.test
+    local = cmfb.Triples(te.user - ub[rank], te.item, te.rating)
+    sse = cmfb.rmse(x, th, local) ** 2 * len(te)
+    return x.cpu().numpy(), th.cpu().numpy(), sse, len(te)
+
+
+def _worker_rs(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, th, sse, cnt = _run_rs(rank, world)
+        np.savez(f"{out}_{rank}.npz", x=x, th=th, sse=sse, cnt=cnt)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reduce_scatter_exchange(tmp_path):
+    """world = 1: the reduce-scatter route (pass 1 -> partial -> pass 2) equals
+    the replicated engine bit for bit (the partial is the full fp32
+    accumulator).  world = 2 (gloo, one device): X sharded, partial item Grams
+    summed across ranks -- same factors up to fp32 summation order and the same
+    test RMSE to 1e-6."""
+    import paper_1808_03843_b200 as cmfb
+    from paper_1808_03843_b200.distributed import ShardedALS
+    m, n, nnz = SHAPE
+    x1, th1, sse1, cnt1 = _run_rs(0, 1)
+    # the replicated single-rank engine on the same matrix
+    full, _ = cmfb.gen_synthetic_stream(m, n, F, nnz, 0.1, 0.1, 3)
+    eng = ShardedALS(full, F, lam=0.05, solver=cmfb.SolverConfig("cg", precision="fp16"))
+    x = torch.from_numpy(cmfb.init_factors(m, F, 0.1, [0, 0])).cuda()
+    th = torch.from_numpy(cmfb.init_factors(n, F, 0.1, [0, 1])).cuda()
+    for _ in range(ITERS):
+        eng.iteration(x, th)
+    assert np.array_equal(x.cpu().numpy(), x1) and np.array_equal(th.cpu().numpy(), th1)
+    out = str(tmp_path / "rs")
+    mp.spawn(_worker_rs, args=(2, _free_port(), out), nprocs=2, join=True)
+    parts = [np.load(f"{out}_{r}.npz") for r in range(2)]
+    x2 = np.concatenate([p["x"] for p in parts])
+    assert np.array_equal(parts[0]["th"], parts[1]["th"])
+    rel = np.linalg.norm(x2 - x1) / np.linalg.norm(x1)
+    assert rel < 1e-4, rel
+    rmse1 = np.sqrt(sse1 / cnt1)
+    rmse2 = np.sqrt(sum(float(p["sse"]) for p in parts) / sum(int(p["cnt"]) for p in parts))
+    assert abs(rmse2 - rmse1) < 1e-6
