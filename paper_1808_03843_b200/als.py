@@ -242,6 +242,8 @@ class HalfUpdatePlan:
             else:
                 nat.call("cmf_fused_cg_update_ws", *common, nat.ptr(peers) if npeers else None, npeers,
                          tail[0], tail[1], tail[2], tail[3], nat.ptr(ws), wsb, tail[4])
+            if ws is not None and f <= 104:
+                nat.LAUNCHES[0] += 2  # two passes: the segment split + the second fused launch
             if record is not None:
                 e1.record()
                 record.setdefault("fused_tc_cg", []).append((e0, e1))
