@@ -456,7 +456,7 @@ __device__ void gather_weighted(const GatherArgs &g, const __half *fixed16, int 
 }
 
 #ifndef CMF_SCALE_BATCH
-#define CMF_SCALE_BATCH 1
+#define CMF_SCALE_BATCH 4
 #endif
 template <int NST, int NBUF>
 __device__ void scale_weighted(const GatherArgs &g, int W, float alpha, const Pipe<NST, true, NBUF> &pp,
@@ -466,7 +466,6 @@ __device__ void scale_weighted(const GatherArgs &g, int W, float alpha, const Pi
     cur.first(row0);
     cur.advance(pw);
     const int c = lane & 15, hrow = lane >> 4;
-    const bool live = c < (W >> 3);
     uint32_t dst_off[4];
 #pragma unroll
     for (int t4 = 0; t4 < 4; ++t4) dst_off[t4] = operand_addr(0, 2 * t4 + hrow, c);
@@ -489,9 +488,13 @@ __device__ void scale_weighted(const GatherArgs &g, int W, float alpha, const Pi
         mbar_wait_backoff(pp.empty(s), ((it / NST) & 1) ^ 1);
         mbar_wait(landed + 8u * s, (it / NST) & 1);  // the gathered rows of stage it are in
         if (lane == 0 && it < TRACE_STAGES) trace_at(g.trace, 8 * it + 5);
-        // SB row pairs at a time: all loads first, then the
-        // products and stores (a load -> multiply -> store chain per chunk would
-        // serialise on the shared-memory latency)
+        // the weights as replicated binary16 pairs, one conversion per rating
+        const __half2 hw0 = __float2half2_rn(alpha * pv0), hw1 = __float2half2_rn(alpha * pv1);
+        const uint32_t w0 = *reinterpret_cast<const uint32_t *>(&hw0), w1 = *reinterpret_cast<const uint32_t *>(&hw1);
+        // SB row pairs at a time, all loads first.  No lane predicate: the lanes
+        // past the shadow width (chunks c >= W/8) scale stale chunks into operand
+        // rows >= W that feed only accumulator columns the repack discards (rows
+        // W, W+1 are rewritten below), which keeps the loop free of branches.
 #pragma unroll
         for (int t0 = 0; t0 < KS / 2; t0 += SB) {
             if ((t0 & 7) == 0 && 2 * t0 >= n16) break;
@@ -499,30 +502,25 @@ __device__ void scale_weighted(const GatherArgs &g, int W, float alpha, const Pi
 #pragma unroll
             for (int k = 0; k < SB; ++k) {
                 const uint32_t off = dst_off[(t0 + k) & 3] + ((t0 + k) >> 2) * KBLK_BYTES;
-                if (live)
-                    asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                        : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
-                        : "r"(stg + off));
+                asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
+                             : "r"(stg + off));
             }
 #pragma unroll
             for (int k = 0; k < SB; ++k) {
                 const int t = t0 + k;
-                const float r = __shfl_sync(0xffffffffu, t < 16 ? pv0 : pv1, (2 * t + hrow) & 31);
-                const __half2 w2 = __float2half2_rn(alpha * r);
-                if (live) {
-                    const uint32_t off = dst_off[t & 3] + (t >> 2) * KBLK_BYTES;
-                    const uint32_t w = *reinterpret_cast<const uint32_t *>(&w2);
-                    auto mul = [&](uint32_t x) {
-                        __half2 y =
-                            __hmul2(*reinterpret_cast<const __half2 *>(&x), *reinterpret_cast<const __half2 *>(&w));
-                        return *reinterpret_cast<const uint32_t *>(&y);
-                    };
-                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(wst + off), "r"(mul(v[k].x)),
-                                 "r"(mul(v[k].y)), "r"(mul(v[k].z)), "r"(mul(v[k].w))
-                                 : "memory");
-                }
+                const uint32_t w = __shfl_sync(0xffffffffu, t < 16 ? w0 : w1, (2 * t + hrow) & 31);
+                const uint32_t off = dst_off[t & 3] + (t >> 2) * KBLK_BYTES;
+                auto mul = [&](uint32_t x) {
+                    __half2 y = __hmul2(*reinterpret_cast<const __half2 *>(&x), *reinterpret_cast<const __half2 *>(&w));
+                    return *reinterpret_cast<const uint32_t *>(&y);
+                };
+                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(wst + off), "r"(mul(v[k].x)),
+                             "r"(mul(v[k].y)), "r"(mul(v[k].z)), "r"(mul(v[k].w))
+                             : "memory");
             }
         }
+        __syncwarp();  // the stale-chunk stores above land before the rating rows
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float wv = alpha * (h ? pv1 : pv0);
