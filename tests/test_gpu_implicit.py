@@ -134,6 +134,33 @@ def test_implicit_fused_matches_two_step(golden, cuda_device):
     assert np.all(np.isfinite(xa[-3:])) and np.abs(xa[-3:]).max() < np.abs(x0[-3:]).max()
 
 
+@pytest.mark.parametrize("f", [8, 13, 32, 57, 100, 120])
+@pytest.mark.parametrize("side", ["short", "long"])
+def test_implicit_fused_matches_two_step_over_widths(cuda_device, f, side):
+    """The fused weighted kernel against the two-step route across the template
+    buckets (shadow widths W = 8 .. 120, so the lanes past W/8 16-byte chunks
+    differ per f) on short rows (the user-side instance) and on long rows (the
+    item-side instance, >= 1024 ratings per row)."""
+    rng = np.random.default_rng(f)
+    m, n, k = (400, 500, 30_000) if side == "short" else (3_000, 24, 40_000)
+    u = rng.integers(0, m, k)
+    v = rng.integers(0, n, k)
+    r = rng.integers(1, 6, k).astype(np.float32)
+    sr = cmfb.build(cmfb.Triples(u, v, r), m, n)
+    # short: user rows (~75 ratings) over item factors; long: item rows
+    # (~1,667 ratings) over user factors
+    view, nfix, ntgt = (sr.csr_view(), n, m) if side == "short" else (sr.csc_view(), m, n)
+    fixed = cmfb.init_factors(nfix, f, 0.1, [0, 1])
+    gram = cmfb.precompute_gram(fixed)
+    x0 = cmfb.init_factors(ntgt, f, 0.1, [0, 0])
+    cfg = cmfb.SolverConfig("cg", 6, 1e-4, "fp16")
+    xa, xb = x0.copy(), x0.copy()
+    cmfb.implicit_update_side(view, fixed, gram, xa, 0.5, 0.05, cfg)
+    cmfb.implicit_update_side(view, fixed, gram, xb, 0.5, 0.05, cfg, gram_kernel="fma")
+    assert np.all(np.isfinite(xa))
+    assert _rel(xa, xb) < 5e-3
+
+
 def _mpr_loop(x, theta, users, items):
     """implicit.py:115-131 restated (float32 scores, ties averaged)."""
     n = theta.shape[0]
