@@ -316,7 +316,9 @@ struct TmemCg {
             sa = NRED >= 1 ? (rd[0] + rd[4]) + (rd[8] + rd[12]) : 0.0f;
             sb = NRED >= 2 ? (rd[16] + rd[20]) + (rd[24] + rd[28]) : 0.0f;
         }
-#elif defined(CMF_RED16)
+#elif !defined(CMF_RED3)
+        // (default; CMF_RED3: every lane sums the 16 partials of each value from
+        // four float4 loads -- 2% slower on the Netflix user side, same-box A/B)
         if (NRED >= 1) {
             // lane l sums partial l & 15 of value l >> 4 with a 16-lane butterfly
             // (bitwise identical in every lane: each level adds the same pair)
