@@ -63,13 +63,16 @@ __device__ __forceinline__ int factor_tile(float4 *tl, int T, float *rd) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(128, 8) chol_smem_kernel(const float *A, int64_t a_stride, const float *B,
+#ifndef CMF_CHOL_NT
+#define CMF_CHOL_NT 128
+#endif
+__global__ void __launch_bounds__(CMF_CHOL_NT, 1024 / CMF_CHOL_NT) chol_smem_kernel(const float *A, int64_t a_stride, const float *B,
                                                           const int64_t *nu, int64_t nsys, int f, float *X,
                                                           int32_t *info, int32_t *nbad) {
     extern __shared__ __align__(16) float csm[];
     const int64_t s = blockIdx.x;
     if (nu && nu[s] == 0) return;
-    constexpr int NT = 128;
+    constexpr int NT = CMF_CHOL_NT;
     const int tid = threadIdx.x;
     const int fp = (f + 3) & ~3, TR = fp >> 2, T = TR * (TR + 1) / 2;
     // shared: tiles | z / y (fp) | 1/L_ii (fp) | panel^T (4 fp) | tile rows I, cols J | flag.
@@ -271,7 +274,7 @@ int chol_smem_launch(const float *a, int64_t a_stride, const float *b, const int
             cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return set_error(CMF_ECUDA, "chol_smem smem attr: %s", cudaGetErrorString(e));
     }
-    chol_smem_kernel<<<static_cast<unsigned>(nsys), 128, smem, st>>>(a, a_stride, b, nu, nsys, f, x, info, nbad);
+    chol_smem_kernel<<<static_cast<unsigned>(nsys), CMF_CHOL_NT, smem, st>>>(a, a_stride, b, nu, nsys, f, x, info, nbad);
     return check_launch("chol_smem_kernel");
 }
 
