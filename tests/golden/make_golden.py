@@ -28,6 +28,9 @@ Fixtures:
   train_f100.npz    1/10-Netflix shape at f=100 (48,019 x 17,770, 9.9M train
                     ratings): the same records as train_ml1m for exact / cg32 /
                     cg16 (run on demand: `make_golden.py f100`, ~40 min here)
+  implicit100.npz   implicit_train at f = 100 (3,000 x 1,500, 148K ratings): cg16
+                    and exact objective / RMSE per epoch, one cg16
+                    implicit_update_side per side (`make_golden.py implicit100`)
   train_ml1m.npz    MovieLens-1M-shaped protocol (BASELINE configs[0]): RMSE and
                     objective per epoch for exact / cg-fp32 / cg-fp16, sampled
                     factor rows per epoch (exact), and SHA-256 digests of the
@@ -424,6 +427,44 @@ def implicit16(cmf):
     np.savez_compressed(os.path.join(OUT, "implicit16.npz"), **out)
 
 
+def implicit100(cmf):
+    """implicit_train at f = 100 (the fused weighted kernel's headline instance,
+    FC = 25) on a non-negative instance with users of ~50 and items of ~100
+    observations: cg16 (alpha = 1) and exact trajectories (objective and
+    preference RMSE per epoch) and one cg16
+    implicit_update_side of each side from the initial factors."""
+    import cmf.implicit as imp
+    m, n, nnz, f = 3000, 1500, 165_000, 100
+    rng = np.random.default_rng(100)
+    flat = np.sort(rng.choice(m * n, size=nnz, replace=False))
+    vals = rng.integers(1, 6, size=nnz).astype(np.float32)
+    t = cmf.Triples((flat // n).astype(np.int64), (flat % n).astype(np.int64), vals)
+    tr, te = cmf.split_holdout(t, 0.1, 7)
+    sr = cmf.build(tr, m, n)
+    out = {"meta": np.array([m, n, f], np.int64), "alpha": np.array(1.0)}
+    for name, a in (("row_ptr", sr.row_ptr), ("col_idx", sr.col_idx), ("csr_val", sr.csr_val),
+                    ("col_ptr", sr.col_ptr), ("row_idx", sr.row_idx), ("csc_val", sr.csc_val)):
+        out[name] = a
+    out["te_u"], out["te_v"], out["te_r"] = te.user, te.item, te.rating
+    cfg = cmf.SolverConfig("cg", 6, 1e-4, "fp16")
+    x0 = cmf.init_factors(m, f, 0.1, [0, 0])
+    t0 = cmf.init_factors(n, f, 0.1, [0, 1])
+    x1 = x0.copy()
+    imp.implicit_update_side(sr.csr_view(), t0, imp.precompute_gram(t0), x1, 1.0, 0.05, cfg)
+    t1 = t0.copy()
+    imp.implicit_update_side(sr.csc_view(), x0, imp.precompute_gram(x0), t1, 1.0, 0.05, cfg)
+    out["x1_cg16"], out["t1_cg16"] = x1, t1
+    X, T, rep = imp.implicit_train(sr, imp.ImplicitConfig(f=f, alpha=1.0, lam=0.05, epochs=3, solver=cfg), te)
+    out["cg16_obj"] = np.array([e.objective for e in rep.epochs])
+    out["cg16_rmse"] = np.array([e.rmse for e in rep.epochs])
+    X, T, rep = imp.implicit_train(sr, imp.ImplicitConfig(f=f, alpha=1.0, lam=0.05, epochs=3,
+                                                          solver=cmf.SolverConfig("exact")), te)
+    out["exact_obj"] = np.array([e.objective for e in rep.epochs])
+    out["exact_rmse"] = np.array([e.rmse for e in rep.epochs])
+    print("implicit100", out["cg16_obj"], out["cg16_rmse"], out["exact_obj"], out["exact_rmse"])
+    np.savez_compressed(os.path.join(OUT, "implicit100.npz"), **out)
+
+
 def io_cases(cmf):
     out = {}
     rng = np.random.default_rng(21)
@@ -456,5 +497,6 @@ if __name__ == "__main__":
     for w in which:
         {"gram": gram_cases, "solve": solve_cases, "build": build_cases,
          "data": data_cases, "small": train_small, "implicit": implicit_small,
-         "io": io_cases, "ml1m": train_ml1m, "f100": train_f100, "implicit16": implicit16}[w](cmf)
+         "io": io_cases, "ml1m": train_ml1m, "f100": train_f100, "implicit16": implicit16,
+         "implicit100": implicit100}[w](cmf)
         print("wrote", w)

@@ -134,6 +134,32 @@ def test_implicit_fused_matches_two_step(golden, cuda_device):
     assert np.all(np.isfinite(xa[-3:])) and np.abs(xa[-3:]).max() < np.abs(x0[-3:]).max()
 
 
+def test_implicit_f100_vs_reference(golden, cuda_device):
+    """The weighted fused kernel at the headline width (f = 100, FC = 25 on both
+    the user and the item instance) against the reference's own cg16 route
+    (tests/golden/implicit100.npz): one half-update per side, then a 3-epoch
+    implicit_train trajectory within the 1e-3 RMSE bar."""
+    g = golden("implicit100")
+    m, n, f = (int(v) for v in g["meta"])
+    sr = cmfb.SparseRatings(m, n, int(g["row_ptr"][-1]), g["row_ptr"], g["col_idx"], g["csr_val"],
+                            g["col_ptr"], g["row_idx"], g["csc_val"])
+    te = cmfb.Triples(g["te_u"], g["te_v"], g["te_r"])
+    cfg = cmfb.SolverConfig("cg", 6, 1e-4, "fp16")
+    x0 = cmfb.init_factors(m, f, 0.1, [0, 0])
+    t0 = cmfb.init_factors(n, f, 0.1, [0, 1])
+    x1 = x0.copy()
+    cmfb.implicit_update_side(sr.csr_view(), t0, cmfb.precompute_gram(t0), x1, 1.0, 0.05, cfg)
+    assert _rel(x1, g["x1_cg16"]) < 5e-3
+    t1 = t0.copy()
+    cmfb.implicit_update_side(sr.csc_view(), x0, cmfb.precompute_gram(x0), t1, 1.0, 0.05, cfg)
+    assert _rel(t1, g["t1_cg16"]) < 5e-3
+    X, T, rep = cmfb.implicit_train(sr, cmfb.ImplicitConfig(f=f, alpha=1.0, lam=0.05, epochs=3, solver=cfg), te)
+    rmse = np.array([e.rmse for e in rep.epochs])
+    obj = np.array([e.objective for e in rep.epochs])
+    assert np.abs(rmse - g["cg16_rmse"]).max() < 1e-3
+    assert np.allclose(obj, g["cg16_obj"], rtol=1e-3)
+
+
 @pytest.mark.parametrize("f", [8, 13, 32, 57, 100, 120])
 @pytest.mark.parametrize("side", ["short", "long"])
 def test_implicit_fused_matches_two_step_over_widths(cuda_device, f, side):
