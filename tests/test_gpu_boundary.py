@@ -134,3 +134,32 @@ def test_predict_pairs_bitwise_equal_to_reference_einsum(cuda_device, f):
     assert np.array_equal(got, want)
     t, truth = cmfb.gen_synthetic(40, 30, f, 0.3, 0.0, seed=1)
     assert cmfb.rmse(truth.x_true, truth.theta_true, t) == 0.0
+
+
+def _one_heavy_user(n_items=700, f=100, value=1.0, n_light=2000):
+    """User 0 rates n_items items whose factors are all `value` (A_u entries
+    n_items * value^2); n_light users with 3 ratings each keep the view's mean
+    row short, so the user side runs the short-row CTA shape."""
+    rng = np.random.default_rng(11)
+    u = np.concatenate([np.zeros(n_items, np.int64), np.repeat(np.arange(1, n_light + 1), 3)])
+    i = np.concatenate([np.arange(n_items), rng.integers(0, n_items, 3 * n_light)])
+    t = cmfb.Triples(u, i, np.full(u.size, 3.0, np.float32))
+    sr = cmfb.build(t, n_light + 1, n_items)
+    theta = np.full((n_items, f), value, np.float32)
+    x = np.zeros((n_light + 1, f), np.float32)
+    return sr, theta, x
+
+
+def test_short_row_overflow(cuda_device):
+    """Short-row views (the user side's 4-group CTA shape): one heavy user's A_u
+    just inside the binary16 range (700 * 9.3^2 = 60,543) solves, just past it
+    (700 * 9.7^2 = 65,863) raises NumericalError like pack_half."""
+    cg16 = cmfb.SolverConfig("cg", 6, 1e-4, "fp16")
+    sr, theta, x = _one_heavy_user(value=9.3)
+    assert sr.nnz < 1024 * sr.m
+    cmfb.update_side(sr.csr_view(), theta, x, 0.05, cg16)
+    assert np.all(np.isfinite(x))
+    sr, theta, x = _one_heavy_user(value=9.7)
+    with pytest.raises(cmfb.NumericalError, match="rescale"):
+        cmfb.update_side(sr.csr_view(), theta, x, 0.05, cg16)
+
