@@ -107,6 +107,23 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
                          int32_t weighted_reg, const float *base_packed, int32_t precision,
                          void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
                          int32_t *overflow_flag, void *stream);
+/*
+ * cmf_gram_assemble_tc with the rows' rating count and a device workspace:
+ * the split-precision (fp32) Gram over long rows (nnz >= 1024 * nrows) whose
+ * hi + lo shadow exceeds 56 MB runs P <= 8 passes over equal fixed-side id
+ * ranges (each pass's shadow slice stays in L2), accumulating into a_out /
+ * b_out; P - 1 arrays of nrows int64 segment bounds go to `ws`
+ * (cmf_gram_tc_workspace_bytes; too small or NULL: one pass).  Same results as
+ * cmf_gram_assemble_tc up to fp32 summation order.  No base_packed.
+ * Replaces the same reference path (gram.py:161-236 assemble_side).
+ */
+int cmf_gram_assemble_tc_ws(const int64_t *indptr, const int32_t *indices, const float *b_weights,
+                            int64_t nrows, int64_t nnz, const void *fixed16, const void *fixed16_lo,
+                            int64_t ncols, float split_scale, int32_t w16, int32_t f, double lam,
+                            int32_t weighted_reg, int32_t precision, void *a_out, int64_t a_stride,
+                            float *b_out, int64_t *nu_out, int32_t *overflow_flag, void *ws,
+                            int64_t ws_bytes, void *stream);
+int64_t cmf_gram_tc_workspace_bytes(int64_t nrows, int64_t nnz, int64_t ncols, int32_t f, int32_t split);
 /* hi = fp16(scale*x), lo = fp16(scale*x - hi), both (rows + 1, w16), zero padded
  * (row `rows` all zero, as cmf_factors_to_half);
  * a finite value whose hi overflows binary16 sets *overflow_flag. */

@@ -37,6 +37,9 @@ _SIGNATURES = {
                                          _vp, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
     "cmf_gram_assemble_tc": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_float, _i32, _i32,
                                             _f64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "cmf_gram_assemble_tc_ws": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, ctypes.c_float, _i32,
+                                               _i32, _f64, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
+    "cmf_gram_tc_workspace_bytes": (ctypes.c_int64, [_i64, _i64, _i64, _i32, _i32]),
     "cmf_factors_to_half_split": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _i32, ctypes.c_float,
                                                  _vp, _vp]),
     "cmf_tc_width": (ctypes.c_int, [_i32]),
@@ -140,7 +143,7 @@ def check(rc: int, what: str = ""):
 
 # Kernel-launching entry points called since the counter was last reset (the
 # benchmark's "gpu_launches" claim counts launches of OUR kernels).
-_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_fused_cg_update_ws": 1, "cmf_fused_cg_update_implicit": 1, "cmf_fused_cg_pass": 1, "cmf_dense_gram": 2, "cmf_implicit_loss_csr": 2, "cmf_group_rows": 6, "cmf_mpr_count": 1, "cmf_gen_truth": 1, "cmf_gen_count": 3, "cmf_gen_fill": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
+_LAUNCH_COST = {"cmf_factors_to_half_split": 1, "cmf_fused_cg_update": 1, "cmf_fused_cg_update_peers": 1, "cmf_fused_cg_update_ws": 1, "cmf_fused_cg_update_implicit": 1, "cmf_fused_cg_pass": 1, "cmf_dense_gram": 2, "cmf_implicit_loss_csr": 2, "cmf_group_rows": 6, "cmf_mpr_count": 1, "cmf_gen_truth": 1, "cmf_gen_count": 3, "cmf_gen_fill": 1, "cmf_gram_assemble": 1, "cmf_gram_assemble_tc": 1, "cmf_gram_assemble_tc_ws": 1, "cmf_factors_to_half": 1, "cmf_spmm_bias": 1, "cmf_batch_cg": 1,
                 "cmf_batch_cholesky": 1, "cmf_pack_half": 1, "cmf_sq_error": 2,
                 "cmf_sq_error_csr": 2, "cmf_weighted_sqnorm": 2, "cmf_predict_pairs": 1}
 LAUNCHES = [0]

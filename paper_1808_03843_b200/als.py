@@ -254,7 +254,21 @@ class HalfUpdatePlan:
             if record is not None:
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record()
-            if tc:
+            if tc and lo is not None:
+                # split-precision (fp32) Gram: long rows over a fixed side whose hi + lo
+                # shadow exceeds L2 run in passes over fixed-side id ranges (the
+                # segment bounds live in a small workspace; see cmf_gram_assemble_tc_ws)
+                nnz_b = (int(values.numel()) if nnz is None else int(nnz)) * nb // max(nrows, 1)
+                wsb = int(nat.lib().cmf_gram_tc_workspace_bytes(nb, nnz_b, fx.shape[0], f, 1))
+                ws = _WS.get(self.dev, wsb, key="gram_passes") if wsb else None
+                nat.call("cmf_gram_assemble_tc_ws", nat.ptr(indptr) + 8 * r0, nat.ptr(indices),
+                         nat.ptr(values), nb, nnz_b, nat.ptr(shadow), lo, fx.shape[0], SPLIT_SCALE, self.w16, f,
+                         float(lam), int(bool(weighted_reg)), nat.PREC[solver.precision],
+                         nat.ptr(self.a_ws), self.stride, nat.ptr(self.b_ws),
+                         nat.ptr(self.nu_ws), nat.ptr(self.flags), nat.ptr(ws), wsb, st)
+                if wsb:  # P passes + P - 1 segment splits
+                    nat.LAUNCHES[0] += 2 * (wsb // (8 * nb))
+            elif tc:
                 nat.call("cmf_gram_assemble_tc", nat.ptr(indptr) + 8 * r0, nat.ptr(indices),
                          nat.ptr(values), nb, nat.ptr(shadow), lo, fx.shape[0], SPLIT_SCALE, self.w16, f,
                          float(lam),

@@ -23,7 +23,11 @@ int gram_simt_launch(const int64_t *, const int32_t *, const float *, const floa
                      float *, int64_t *, int32_t *, cudaStream_t);
 int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, const void *, int64_t,
                    float, int, int, double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
-                   cudaStream_t);
+                   cudaStream_t, const int64_t * = nullptr, const int64_t * = nullptr, int = 0, int = 1);
+int gram_tc_ws_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, const void *, int64_t,
+                      float, int, int, double, int, bool, void *, int64_t, float *, int64_t *, int32_t *, int64_t,
+                      void *, int64_t, cudaStream_t);
+int64_t gram_tc_passes(int64_t nrows, int64_t nnz, int64_t ncols, int W, bool split);
 int factors_to_half_split_launch(const float *, int64_t, int, void *, void *, int, float, int32_t *, cudaStream_t);
 int gram_tc_width(int f);
 int fused_cg_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, int64_t, int, int, double,
@@ -210,6 +214,29 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
     return gram_tc_launch(indptr, indices, b_weights, nrows, fixed16, fixed16_lo, ncols, split_scale, w16, f, lam,
                           weighted_reg, base_packed, precision == CMF_PREC_FP16, a_out, a_stride, b_out, nu_out,
                           overflow_flag, S(stream));
+}
+
+int cmf_gram_assemble_tc_ws(const int64_t *indptr, const int32_t *indices, const float *b_weights,
+                            int64_t nrows, int64_t nnz, const void *fixed16, const void *fixed16_lo, int64_t ncols,
+                            float split_scale, int32_t w16, int32_t f, double lam, int32_t weighted_reg,
+                            int32_t precision, void *a_out, int64_t a_stride, float *b_out, int64_t *nu_out,
+                            int32_t *overflow_flag, void *ws, int64_t ws_bytes, void *stream) {
+    REQUIRE(nrows >= 0 && f >= 1 && nnz >= 0, "bad dimensions");
+    REQUIRE(precision == CMF_PREC_FP32 || precision == CMF_PREC_FP16, "unknown precision %d", precision);
+    REQUIRE(a_stride >= f * (int64_t)(f + 1) / 2, "a_stride smaller than f*(f+1)/2");
+    if (nrows == 0) return CMF_OK;
+    REQUIRE(indptr && a_out && fixed16, "null argument");
+    REQUIRE(!fixed16_lo || split_scale > 0.0f, "split_scale must be > 0");
+    REQUIRE(ncols >= 1, "ncols must be >= 1");
+    REQUIRE(ws_bytes >= 0, "negative workspace size");
+    return gram_tc_ws_launch(indptr, indices, b_weights, nrows, fixed16, fixed16_lo, ncols, split_scale, w16, f, lam,
+                             weighted_reg, precision == CMF_PREC_FP16, a_out, a_stride, b_out, nu_out, overflow_flag,
+                             nnz, ws, ws_bytes, S(stream));
+}
+
+int64_t cmf_gram_tc_workspace_bytes(int64_t nrows, int64_t nnz, int64_t ncols, int32_t f, int32_t split) {
+    if (nrows <= 0) return 0;
+    return (gram_tc_passes(nrows, nnz, ncols, gram_tc_width(f), split != 0) - 1) * nrows * 8;
 }
 
 int cmf_fused_cg_update(const int64_t *indptr, const int32_t *indices, const float *values,

@@ -225,6 +225,15 @@ __global__ void segment_split_kernel(const int64_t *indptr, const int32_t *indic
     }
 }
 
+int segment_split_launch(const int64_t *indptr, const int32_t *indices, int64_t nrows, int32_t split, int64_t *seg,
+                         cudaStream_t st) {
+    if (nrows == 0) return CMF_OK;
+    const int64_t blocks = (nrows + 255) / 256;
+    segment_split_kernel<<<static_cast<unsigned>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(indptr, indices, nrows,
+                                                                                               split, seg);
+    return check_launch("segment_split_kernel");
+}
+
 // Two passes pay when the rows are long (the partial accumulator's HBM round
 // trip, ~2 x 43 KB per row at f = 100, is small against the row's gather) and
 // the fixed side's binary16 shadow is too large to stay in L2 across the

@@ -30,6 +30,8 @@
 //              accumulate), tcgen05.commit -> empty[s] / tmem_full[b].
 // Two TMEM accumulators (2 x 128 columns) let the epilogue of row u overlap
 // the MMAs of row u+1.
+#include <climits>
+#include <cstdlib>
 #include <type_traits>
 
 #include "tc_common.cuh"
@@ -54,6 +56,9 @@ struct Args {
     float *b_out;
     int64_t *nu_out;
     int32_t *overflow;
+    // multi-pass (gather.pass 3): add this pass's Gram / bias to a_out / b_out
+    // (fp32 only), and lambda*n_u on the diagonal only in the last pass
+    int accumulate, add_reg;
 };
 
 __device__ __forceinline__ void bar_epi() { named_bar(1, EPI_THREADS); }
@@ -116,8 +121,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
         for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
             const int64_t p0 = ga.indptr[u], p1 = ga.indptr[u + 1];
             const int64_t n_u = p1 - p0;
-            const float reg = g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
-                                         : __double2float_rn(g.lam);
+            const float reg = !g.add_reg ? 0.0f
+                              : g.weighted ? __double2float_rn(g.lam * static_cast<double>(n_u))
+                                           : __double2float_rn(g.lam);
             float bias = 0.0f, diag = 0.0f;
             if (n_u == 0) {
                 if (i < f)
@@ -127,10 +133,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
                 mbar_wait(pp.tfull(b), (rowc >> 1) & 1);
                 tc_fence_after();
                 const uint32_t tbase = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + b * g.N;
+                // a pass whose segment of this row is empty: the MMA warp committed
+                // the buffer untouched (stale), so its contribution is zero
+                bool seg_acc = true;
+                if (ga.pass) {
+                    int64_t s0, s1;
+                    row_segment(ga, u, s0, s1);
+                    seg_acc = s1 > s0;
+                }
                 for (int cc = 0; cc < nchunk; ++cc) {
                     uint32_t v[32];
                     tmem_ld32(tbase + cc * 32, v);
                     tmem_ld_wait();
+                    if (!seg_acc) {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) v[jj] = 0u;
+                    }
                     const int c0 = cc * 32;
                     if (SPLIT) {
 #pragma unroll
@@ -180,7 +198,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
                 sq_row[i] = static_cast<SqT>(dv);
                 if (HALF_OUT) ovf_max = fmaxf(ovf_max, fabsf(dv));
             }
-            if (g.b_out && i < f) g.b_out[u * f + i] = bias;
+            if (g.b_out && i < f) g.b_out[u * f + i] = g.accumulate ? g.b_out[u * f + i] + bias : bias;
             if (tid == 0 && g.nu_out) g.nu_out[u] = n_u;
             bar_epi();
             // packed copy-out: entries k..k+3 per step (k % 4 == 0)
@@ -202,8 +220,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
                             w.y = *reinterpret_cast<uint32_t *>(&c);
                             *reinterpret_cast<uint2 *>(dst) = w;
                         } else {
-                            *reinterpret_cast<float4 *>(dst) = make_float4(e0, e1, e2, e3);
+                            float4 o = make_float4(static_cast<float>(e0), static_cast<float>(e1),
+                                                   static_cast<float>(e2), static_cast<float>(e3));
+                            if (g.accumulate) {
+                                const float4 q = *reinterpret_cast<const float4 *>(dst);
+                                o = make_float4(q.x + static_cast<float>(e0), q.y + static_cast<float>(e1),
+                                                q.z + static_cast<float>(e2), q.w + static_cast<float>(e3));
+                            }
+                            *reinterpret_cast<float4 *>(dst) = o;
                         }
+                    } else if (g.accumulate) {
+                        dst[0] = static_cast<SqT>(static_cast<float>(dst[0]) + static_cast<float>(e0));
+                        if (nk > 1) dst[1] = static_cast<SqT>(static_cast<float>(dst[1]) + static_cast<float>(e1));
+                        if (nk > 2) dst[2] = static_cast<SqT>(static_cast<float>(dst[2]) + static_cast<float>(e2));
+                        if (nk > 3) dst[3] = static_cast<SqT>(static_cast<float>(dst[3]) + static_cast<float>(e3));
                     } else {
                         dst[0] = e0;
                         if (nk > 1) dst[1] = e1;
@@ -352,7 +382,8 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
                    const void *fixed16, const void *fixed16_lo, int64_t ncols, float split_scale, int W, int f,
                    double lam,
                    int weighted, const float *base, bool half, void *a_out, int64_t a_stride, float *b_out,
-                   int64_t *nu_out, int32_t *overflow, cudaStream_t st) {
+                   int64_t *nu_out, int32_t *overflow, cudaStream_t st, const int64_t *seg,
+                   const int64_t *seg_end, int accumulate, int add_reg) {
     if (nrows == 0) return CMF_OK;
     if (W + 2 > tc::M)
         return set_error(CMF_EINVAL, "tensor-core Gram supports f <= %d (got %d)", tc::M - 8, f);
@@ -387,6 +418,14 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     g.nu_out = nu_out;
     g.overflow = overflow;
     g.gather.overflow = overflow;
+    if (seg) {
+        if (!split || half || base) return set_error(CMF_EINVAL, "multi-pass Gram: split fp32 output only");
+        g.gather.pass = 3;
+        g.gather.seg = seg;
+        g.gather.seg_end = seg_end;
+    }
+    g.accumulate = accumulate;
+    g.add_reg = add_reg;
     const int64_t P = packed_size(f);
     const size_t sq_bytes = ((static_cast<size_t>(f) * W * esz) + 15) & ~static_cast<size_t>(15);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
@@ -400,6 +439,54 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     }
     return half ? dispatch_nch<true, false>(nch, g, smem, nrows, st)
                 : dispatch_nch<false, false>(nch, g, smem, nrows, st);
+}
+
+}  // namespace cmf
+
+namespace cmf {
+
+int segment_split_launch(const int64_t *indptr, const int32_t *indices, int64_t nrows, int32_t split, int64_t *seg,
+                         cudaStream_t st);
+
+// Split-precision (fp32) Gram over long rows whose fixed side's hi + lo shadow
+// is larger than L2 keeps (the Netflix item side of the exact route: 200 MB of X
+// shadow, 51% L2 hits and 28.5 GB of DRAM reads in one pass): P passes over
+// equal user-id ranges, each gathering from a ~1/P slice of the shadow; pass 1
+// writes A / b, later passes add to them, the last adds lambda*n_u.  The
+// per-row segment bounds (P - 1 arrays of nrows int64) live in ws.
+int64_t gram_tc_passes(int64_t nrows, int64_t nnz, int64_t ncols, int W, bool split) {
+    if (const char *e = getenv("CMF_GRAM_PASSES"))  // A/B and tests (empty: automatic)
+        if (*e) return atoi(e) > 1 ? (atoi(e) < 16 ? atoi(e) : 16) : 1;
+    const int64_t shadow = ncols * W * 2 * (split ? 2 : 1);
+    if (!split || nnz < 1024 * nrows || shadow <= (int64_t(56) << 20)) return 1;
+    const int64_t p = (shadow + (int64_t(56) << 20) - 1) / (int64_t(56) << 20);
+    return p < 8 ? p : 8;
+}
+
+int gram_tc_ws_launch(const int64_t *indptr, const int32_t *indices, const float *values, int64_t nrows,
+                      const void *fixed16, const void *fixed16_lo, int64_t ncols, float split_scale, int W, int f,
+                      double lam, int weighted, bool half, void *a_out, int64_t a_stride, float *b_out,
+                      int64_t *nu_out, int32_t *overflow, int64_t nnz, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    const int64_t P = gram_tc_passes(nrows, nnz, ncols, W, fixed16_lo != nullptr);
+    if (P <= 1 || half || !fixed16_lo || !ws || ws_bytes < (P - 1) * nrows * 8 || ncols > INT32_MAX)
+        return gram_tc_launch(indptr, indices, values, nrows, fixed16, fixed16_lo, ncols, split_scale, W, f, lam,
+                              weighted, nullptr, half, a_out, a_stride, b_out, nu_out, overflow, st, nullptr,
+                              nullptr, 0, 1);
+    int64_t *segs = static_cast<int64_t *>(ws);
+    for (int64_t k = 1; k < P; ++k) {
+        const int rc = segment_split_launch(indptr, indices, nrows, static_cast<int32_t>(ncols * k / P),
+                                            segs + (k - 1) * nrows, st);
+        if (rc != CMF_OK) return rc;
+    }
+    for (int64_t k = 1; k <= P; ++k) {
+        const int64_t *b = k == 1 ? indptr : segs + (k - 2) * nrows;
+        const int64_t *e = k == P ? indptr + 1 : segs + (k - 1) * nrows;
+        const int rc = gram_tc_launch(indptr, indices, values, nrows, fixed16, fixed16_lo, ncols, split_scale, W, f,
+                                      lam, weighted, nullptr, half, a_out, a_stride, b_out, nu_out, overflow, st, b,
+                                      e, k > 1, k == P);
+        if (rc != CMF_OK) return rc;
+    }
+    return CMF_OK;
 }
 
 }  // namespace cmf

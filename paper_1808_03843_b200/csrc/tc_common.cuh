@@ -166,6 +166,8 @@ struct GatherArgs {
     // indptr[u+1]); pass 0 (default) the whole row.
     const int64_t *seg;
     int pass;
+    // pass 3 (multi-pass split Gram, gram_tc.cu): positions [seg[u], seg_end[u])
+    const int64_t *seg_end;
 };
 
 // Gather range of row u in the current pass.
@@ -174,6 +176,10 @@ __device__ __forceinline__ void row_segment(const GatherArgs &g, int64_t u, int6
     e = g.indptr[u + 1];
     if (g.pass == 1) e = g.seg[u];
     else if (g.pass == 2) b = g.seg[u];
+    else if (g.pass == 3) {
+        b = g.seg[u];
+        e = g.seg_end[u];
+    }
 }
 
 // Operand ring of NST stages + NBUF TMEM accumulator hand-offs (mbarriers:

@@ -230,6 +230,36 @@ def test_exact_route_long_rows_factor_bar(oracle, cuda_device):
         assert np.linalg.norm(t_g - t_o) / np.linalg.norm(t_o) < 1e-4, (epoch, "t")
 
 
+@pytest.mark.parametrize("passes", ["2", "3", "5"])
+def test_exact_route_multipass_gram(oracle, cuda_device, monkeypatch, passes):
+    """The split-precision Gram in P passes over fixed-side id ranges
+    (cmf_gram_assemble_tc_ws: the exact route's item side, whose hi + lo shadow
+    exceeds L2) against one pass and against the CPU oracle: items rated only
+    inside one id range (empty segments in the other passes) and items without
+    ratings included; factors within 1e-4 of the oracle, one pass vs P passes
+    to fp32 summation order."""
+    m, n, f = 1500, 300, 48
+    t, _, _ = oracle.gen_synthetic(m, n, f, 0.5, 0.1, 4)
+    keep = ~((t.item < 20) & (t.user >= m // 3)) & ~((t.item >= 20) & (t.item < 30)) & (t.item != 31)
+    t = oracle.OTriples(t.user[keep], t.item[keep], t.rating[keep])
+    r = oracle.build(t, m, n)
+    x = oracle.init_factors(m, f, 0.1, [0, 0])
+    th0 = oracle.init_factors(n, f, 0.1, [0, 1])
+    sr = cmfb.build(cmfb.Triples(t.user, t.item, t.rating), m, n)
+    solver = cmfb.SolverConfig("exact")
+    th_o = th0.copy()
+    oracle.update_side(r.csc(), x, th_o, 0.05, "exact")
+    outs = []
+    for p in ("1", passes):
+        monkeypatch.setenv("CMF_GRAM_PASSES", p)
+        th = th0.copy()
+        cmfb.update_side(sr.csc_view(), x, th, 0.05, solver)
+        outs.append(th)
+    assert np.array_equal(outs[1][31], th0[31])  # no ratings: untouched
+    assert np.linalg.norm(outs[1] - outs[0]) / np.linalg.norm(outs[0]) < 1e-5
+    assert np.linalg.norm(outs[1] - th_o) / np.linalg.norm(th_o) < 1e-4
+
+
 def test_fused_two_pass_item_side_matches_one_pass(cuda_device, monkeypatch):
     """Long rows over a fixed side whose binary16 shadow exceeds L2 (the Netflix
     item side): the fused kernel gathers the first half of the user ids, parks
