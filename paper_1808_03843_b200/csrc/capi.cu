@@ -23,7 +23,7 @@ int gram_simt_launch(const int64_t *, const int32_t *, const float *, const floa
                      float *, int64_t *, int32_t *, cudaStream_t);
 int gram_tc_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, const void *, int64_t,
                    float, int, int, double, int, const float *, bool, void *, int64_t, float *, int64_t *, int32_t *,
-                   cudaStream_t, const int64_t * = nullptr, const int64_t * = nullptr, int = 0, int = 1);
+                   cudaStream_t, const int64_t * = nullptr, const int64_t * = nullptr, int = 0, int = 1, int = 0);
 int gram_tc_ws_launch(const int64_t *, const int32_t *, const float *, int64_t, const void *, const void *, int64_t,
                       float, int, int, double, int, bool, void *, int64_t, float *, int64_t *, int32_t *, int64_t,
                       void *, int64_t, cudaStream_t);

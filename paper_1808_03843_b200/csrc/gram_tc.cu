@@ -65,23 +65,36 @@ __device__ __forceinline__ void bar_epi() { named_bar(1, EPI_THREADS); }
 
 // Packed-offset table: tab[k] = i*W + j for packed entry k = i*(i+1)/2 + j.
 // Built once per CTA; the epilogue copy-out walks the packed row with it.
-template <int NCH, bool HALF_OUT, bool SPLIT>
+// SYM (split operands, long rows): the MMAs build H H^T and S = H^T L in two
+// accumulators (two operand reads per K-step instead of three: the tensor core's
+// shared-memory operand reads set the split Gram's pace); the staging keeps
+// H H^T + S in the lower triangle and S in the upper one, and the copy-out adds
+// the transposed entry (tabT), so A = H H^T + S + S^T.  The staging row stride is
+// W + 1 (odd: the transposed reads spread over the banks).
+template <int NCH, bool HALF_OUT, bool SPLIT, bool SYM = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_constant__ Args g) {
+    static_assert(!SYM || (SPLIT && !HALF_OUT), "SYM: split fp32 Gram only");
     using PipeT = Pipe<STAGES, SPLIT, 2>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     constexpr int W = NCH * 8;
+    constexpr int WS = SYM ? W + 1 : W;  // staging row stride
     using SqT = typename std::conditional<HALF_OUT, __half, float>::type;
     const GatherArgs &ga = g.gather;
     const int f = ga.f;
     const int64_t P = packed_size(f);
-    // layout: [stages (1024-aligned) | square staging (f x W, SqT) | offset table | barriers | tmem slot]
+    // layout: [stages (1024-aligned) | square staging (f x WS, SqT; SYM: + a zero slot) | offset table |
+    //          SYM: transposed offset table, S rows W, W+1 (2f floats) | barriers | tmem slot]
     unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     unsigned char *stage_mem = smem;
     SqT *sq = reinterpret_cast<SqT *>(smem + STAGES * PipeT::kStageBytes);
-    const size_t sq_bytes = ((static_cast<size_t>(f) * W * sizeof(SqT)) + 15) & ~static_cast<size_t>(15);
+    const size_t sq_bytes = ((static_cast<size_t>(f) * WS * sizeof(SqT) + (SYM ? 4 : 0)) + 15) & ~static_cast<size_t>(15);
     uint16_t *tab = reinterpret_cast<uint16_t *>(smem + STAGES * PipeT::kStageBytes + sq_bytes);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * PipeT::kStageBytes + sq_bytes + tab_bytes);
+    uint16_t *tabT = tab + tab_bytes / 2;
+    float *sbias = reinterpret_cast<float *>(tabT + (SYM ? tab_bytes / 2 : 0));
+    const size_t sym_bytes = SYM ? tab_bytes + ((static_cast<size_t>(f) * 8 + 15) & ~static_cast<size_t>(15)) : 0;
+    uint64_t *bars =
+        reinterpret_cast<uint64_t *>(smem + STAGES * PipeT::kStageBytes + sq_bytes + tab_bytes + sym_bytes);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + PipeT::kBars);
     PipeT pp{smem_u32(stage_mem), smem_u32(bars)};
 
@@ -90,8 +103,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
     pipe_init(pp, stage_mem, NUM_THREADS, 33, EPI_THREADS);
     for (int i = tid; i < f; i += NUM_THREADS) {
         const int base = i * (i + 1) / 2;
-        for (int j = 0; j <= i; ++j) tab[base + j] = static_cast<uint16_t>(i * W + j);
+        for (int j = 0; j <= i; ++j) {
+            tab[base + j] = static_cast<uint16_t>(i * WS + j);
+            if (SYM) tabT[base + j] = static_cast<uint16_t>(j < i ? j * WS + i : f * WS);  // diagonal: zero slot
+        }
     }
+    if (SYM && tid == 0) sq[f * WS] = SqT(0.0f);
     if (warp == 8) tmem_alloc(smem_u32(tmem_slot), g.tmem_cols);
     fence_proxy_async();
     tc_fence_before();
@@ -103,7 +120,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
     if (warp >= 4 && warp < 8) {
         produce<STAGES, SPLIT, 2>(ga, g.fixed16, g.fixed16_lo, W, pp, warp - 4, 4, lane, blockIdx.x, G);
     } else if (warp == 8) {
-        issue_mma<STAGES, SPLIT, 2>(ga, pp, tmem_base, g.N, blockIdx.x, G);
+        issue_mma<STAGES, SPLIT, 2, false, SYM>(ga, pp, tmem_base, g.N, blockIdx.x, G);
     } else {
         // ------------------------------------------------------------ epilogue
         // (1) thread i (= TMEM lane = matrix row) drains its accumulator row into
@@ -117,7 +134,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
         const int bias_cc = W >> 5, bias_cc1 = (W + 1) >> 5;
         float ovf_max = 0.0f;
         uint32_t rowc = 0;
-        SqT *sq_row = sq + static_cast<size_t>(i) * W;
+        SqT *sq_row = sq + static_cast<size_t>(i) * WS;
+        // SYM: float scale of this lane's S row (rows W, W+1 carry the ratings: bias terms)
+        const float s_scale = (i == W || i == W + 1) ? g.bias_scale : g.gram_scale;
         for (int64_t u = blockIdx.x; u < ga.nrows; u += G) {
             const int64_t p0 = ga.indptr[u], p1 = ga.indptr[u + 1];
             const int64_t n_u = p1 - p0;
@@ -128,11 +147,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
             if (n_u == 0) {
                 if (i < f)
                     for (int j = 0; j < W; ++j) sq_row[j] = static_cast<SqT>(0.0f);
+                if (SYM && (i == W || i == W + 1))
+                    for (int j = 0; j < f; ++j) sbias[(i - W) * f + j] = 0.0f;
             } else {
                 const int b = rowc & 1;
                 mbar_wait(pp.tfull(b), (rowc >> 1) & 1);
                 tc_fence_after();
-                const uint32_t tbase = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + b * g.N;
+                const uint32_t tbase = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + b * g.N * (SYM ? 2 : 1);
                 // a pass whose segment of this row is empty: the MMA warp committed
                 // the buffer untouched (stale), so its contribution is zero
                 bool seg_acc = true;
@@ -142,14 +163,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
                     seg_acc = s1 > s0;
                 }
                 for (int cc = 0; cc < nchunk; ++cc) {
-                    uint32_t v[32];
+                    uint32_t v[32], w[SYM ? 32 : 1];
                     tmem_ld32(tbase + cc * 32, v);
+                    if constexpr (SYM) tmem_ld32(tbase + g.N + cc * 32, w);
                     tmem_ld_wait();
                     if (!seg_acc) {
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) v[jj] = 0u;
+                        if constexpr (SYM) {
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) w[jj] = 0u;
+                        }
                     }
                     const int c0 = cc * 32;
+                    if constexpr (SYM) {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) w[jj] = __float_as_uint(__uint_as_float(w[jj]) * s_scale);
+                        if (i == W || i == W + 1) {  // (L^T r)_j, the bias half that S carries
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj)
+                                if (c0 + jj < f) sbias[(i - W) * f + c0 + jj] = __uint_as_float(w[jj]);
+                        }
+                    }
                     if (SPLIT) {
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) {
@@ -161,14 +196,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
                     if (cc == warp) {  // warp-uniform: this chunk holds every lane's diagonal
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
-                            if (jj == lane) diag = __uint_as_float(v[jj]);
+                            if (jj == lane)
+                                diag = __uint_as_float(v[jj]) + (SYM ? 2.0f * __uint_as_float(w[SYM ? jj : 0]) : 0.0f);
                     }
                     if (cc == bias_cc || cc == bias_cc1) {  // warp-uniform
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
                             if (c0 + jj == W || c0 + jj == W + 1) bias += __uint_as_float(v[jj]);
                     }
-                    if (i < f) {
+                    if (SYM && i < f) {
+                        // lower triangle: H H^T + S; upper: S (read transposed by the copy-out)
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const int j = c0 + jj;
+                            if (j >= W) break;
+                            const float s_ij = __uint_as_float(w[SYM ? jj : 0]);
+                            sq_row[j] = static_cast<SqT>(j <= i ? __uint_as_float(v[jj]) + s_ij : s_ij);
+                        }
+                    } else if (i < f) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             if (c0 + 8 * q >= W) break;
@@ -198,9 +243,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
                 sq_row[i] = static_cast<SqT>(dv);
                 if (HALF_OUT) ovf_max = fmaxf(ovf_max, fabsf(dv));
             }
-            if (g.b_out && i < f) g.b_out[u * f + i] = g.accumulate ? g.b_out[u * f + i] + bias : bias;
             if (tid == 0 && g.nu_out) g.nu_out[u] = n_u;
             bar_epi();
+            if (SYM && i < f) bias += sbias[i] + sbias[f + i];
+            if (g.b_out && i < f) g.b_out[u * f + i] = g.accumulate ? g.b_out[u * f + i] + bias : bias;
             // packed copy-out: entries k..k+3 per step (k % 4 == 0)
             const size_t row_off = static_cast<size_t>(u) * g.a_stride;
             if (!g.base) {
@@ -211,6 +257,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
                     SqT e1 = nk > 1 ? sq[o.x >> 16] : SqT(0.0f);
                     SqT e2 = nk > 2 ? sq[o.y & 0xFFFF] : SqT(0.0f);
                     SqT e3 = nk > 3 ? sq[o.y >> 16] : SqT(0.0f);
+                    if constexpr (SYM) {  // + S^T (the diagonal reads the zero slot)
+                        const uint2 t = *reinterpret_cast<const uint2 *>(tabT + k);
+                        e0 += sq[t.x & 0xFFFF];
+                        if (nk > 1) e1 += sq[t.x >> 16];
+                        if (nk > 2) e2 += sq[t.y & 0xFFFF];
+                        if (nk > 3) e3 += sq[t.y >> 16];
+                    }
                     SqT *dst = static_cast<SqT *>(g.a_out) + row_off + k;
                     if (nk >= 4 && (reinterpret_cast<uintptr_t>(dst) & (4 * sizeof(SqT) - 1)) == 0) {
                         if (HALF_OUT) {
@@ -339,9 +392,9 @@ int factors_to_half_launch(const float *x, int64_t rows, int f, void *out, int W
     return check_launch("factors_to_half_kernel");
 }
 
-template <int NCH, bool H, bool SPLIT>
+template <int NCH, bool H, bool SPLIT, bool SYM>
 static int launch_nch(const tc::Args &g, size_t smem, int64_t nrows, cudaStream_t st) {
-    auto k = tc::gram_tc_kernel<NCH, H, SPLIT>;
+    auto k = tc::gram_tc_kernel<NCH, H, SPLIT, SYM>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return set_error(CMF_ECUDA, "gram_tc smem attr: %s", cudaGetErrorString(e));
     int dev = 0, sms = 148, per_sm = 1;
@@ -356,25 +409,25 @@ static int launch_nch(const tc::Args &g, size_t smem, int64_t nrows, cudaStream_
     return check_launch("gram_tc_kernel");
 }
 
-template <bool H, bool SPLIT>
+template <bool H, bool SPLIT, bool SYM = false>
 static int dispatch_nch(int nch, const tc::Args &g, size_t smem, int64_t nrows, cudaStream_t st) {
     switch (nch) {
-        case 1: return launch_nch<1, H, SPLIT>(g, smem, nrows, st);
-        case 2: return launch_nch<2, H, SPLIT>(g, smem, nrows, st);
-        case 3: return launch_nch<3, H, SPLIT>(g, smem, nrows, st);
-        case 4: return launch_nch<4, H, SPLIT>(g, smem, nrows, st);
-        case 5: return launch_nch<5, H, SPLIT>(g, smem, nrows, st);
-        case 6: return launch_nch<6, H, SPLIT>(g, smem, nrows, st);
-        case 7: return launch_nch<7, H, SPLIT>(g, smem, nrows, st);
-        case 8: return launch_nch<8, H, SPLIT>(g, smem, nrows, st);
-        case 9: return launch_nch<9, H, SPLIT>(g, smem, nrows, st);
-        case 10: return launch_nch<10, H, SPLIT>(g, smem, nrows, st);
-        case 11: return launch_nch<11, H, SPLIT>(g, smem, nrows, st);
-        case 12: return launch_nch<12, H, SPLIT>(g, smem, nrows, st);
-        case 13: return launch_nch<13, H, SPLIT>(g, smem, nrows, st);
-        case 14: return launch_nch<14, H, SPLIT>(g, smem, nrows, st);
-        case 15: return launch_nch<15, H, SPLIT>(g, smem, nrows, st);
-        default: return launch_nch<16, H, SPLIT>(g, smem, nrows, st);
+        case 1: return launch_nch<1, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 2: return launch_nch<2, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 3: return launch_nch<3, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 4: return launch_nch<4, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 5: return launch_nch<5, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 6: return launch_nch<6, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 7: return launch_nch<7, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 8: return launch_nch<8, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 9: return launch_nch<9, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 10: return launch_nch<10, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 11: return launch_nch<11, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 12: return launch_nch<12, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 13: return launch_nch<13, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 14: return launch_nch<14, H, SPLIT, SYM>(g, smem, nrows, st);
+        case 15: return launch_nch<15, H, SPLIT, SYM>(g, smem, nrows, st);
+        default: return launch_nch<16, H, SPLIT, SYM>(g, smem, nrows, st);
     }
 }
 
@@ -383,7 +436,7 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
                    double lam,
                    int weighted, const float *base, bool half, void *a_out, int64_t a_stride, float *b_out,
                    int64_t *nu_out, int32_t *overflow, cudaStream_t st, const int64_t *seg,
-                   const int64_t *seg_end, int accumulate, int add_reg) {
+                   const int64_t *seg_end, int accumulate, int add_reg, int sym) {
     if (nrows == 0) return CMF_OK;
     if (W + 2 > tc::M)
         return set_error(CMF_EINVAL, "tensor-core Gram supports f <= %d (got %d)", tc::M - 8, f);
@@ -408,7 +461,8 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     g.gram_scale = split ? 1.0f / (split_scale * split_scale) : 1.0f;
     g.bias_scale = split ? 1.0f / split_scale : 1.0f;
     g.N = ((W + 2 + 15) / 16) * 16;
-    g.tmem_cols = 2 * g.N <= 256 ? 256 : 512;
+    if (sym && (!split || half || base)) sym = 0;
+    g.tmem_cols = (sym || 2 * g.N > 256) ? 512 : 256;  // SYM: 2 buffers x (H H^T, S)
     g.lam = lam;
     g.weighted = weighted;
     g.base = base;
@@ -427,15 +481,19 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     g.accumulate = accumulate;
     g.add_reg = add_reg;
     const int64_t P = packed_size(f);
-    const size_t sq_bytes = ((static_cast<size_t>(f) * W * esz) + 15) & ~static_cast<size_t>(15);
+    const size_t ws_row = sym ? W + 1 : W;
+    const size_t sq_bytes = ((static_cast<size_t>(f) * ws_row * esz + (sym ? 4 : 0)) + 15) & ~static_cast<size_t>(15);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
+    const size_t sym_bytes = sym ? tab_bytes + ((static_cast<size_t>(f) * 8 + 15) & ~static_cast<size_t>(15)) : 0;
     const size_t stage_bytes = split ? tc::Pipe<tc::STAGES, true, 2>::kStageBytes
                                      : tc::Pipe<tc::STAGES, false, 2>::kStageBytes;
-    const size_t smem = 1024 + tc::STAGES * stage_bytes + sq_bytes + tab_bytes + tc::Pipe<tc::STAGES>::kBars * 8 + 16;
+    const size_t smem =
+        1024 + tc::STAGES * stage_bytes + sq_bytes + tab_bytes + sym_bytes + tc::Pipe<tc::STAGES>::kBars * 8 + 16;
     const int nch = W / 8;
     if (split) {
         if (half) return set_error(CMF_EINVAL, "the split-precision Gram stores fp32");
-        return dispatch_nch<false, true>(nch, g, smem, nrows, st);
+        return sym ? dispatch_nch<false, true, true>(nch, g, smem, nrows, st)
+                   : dispatch_nch<false, true>(nch, g, smem, nrows, st);
     }
     return half ? dispatch_nch<true, false>(nch, g, smem, nrows, st)
                 : dispatch_nch<false, false>(nch, g, smem, nrows, st);
@@ -468,10 +526,15 @@ int gram_tc_ws_launch(const int64_t *indptr, const int32_t *indices, const float
                       double lam, int weighted, bool half, void *a_out, int64_t a_stride, float *b_out,
                       int64_t *nu_out, int32_t *overflow, int64_t nnz, void *ws, int64_t ws_bytes, cudaStream_t st) {
     const int64_t P = gram_tc_passes(nrows, nnz, ncols, W, fixed16_lo != nullptr);
+    // long rows: the split Gram's K-steps dominate and the SYM copy-out's extra
+    // transposed reads are amortised over ~80 stages per row (short rows: ~3)
+    int sym = nnz >= 1024 * nrows;
+    if (const char *e = getenv("CMF_GRAM_SYM"))  // A/B and tests (empty: automatic)
+        if (*e) sym = atoi(e);
     if (P <= 1 || half || !fixed16_lo || !ws || ws_bytes < (P - 1) * nrows * 8 || ncols > INT32_MAX)
         return gram_tc_launch(indptr, indices, values, nrows, fixed16, fixed16_lo, ncols, split_scale, W, f, lam,
                               weighted, nullptr, half, a_out, a_stride, b_out, nu_out, overflow, st, nullptr,
-                              nullptr, 0, 1);
+                              nullptr, 0, 1, sym);
     int64_t *segs = static_cast<int64_t *>(ws);
     for (int64_t k = 1; k < P; ++k) {
         const int rc = segment_split_launch(indptr, indices, nrows, static_cast<int32_t>(ncols * k / P),
@@ -483,7 +546,7 @@ int gram_tc_ws_launch(const int64_t *indptr, const int32_t *indices, const float
         const int64_t *e = k == P ? indptr + 1 : segs + (k - 1) * nrows;
         const int rc = gram_tc_launch(indptr, indices, values, nrows, fixed16, fixed16_lo, ncols, split_scale, W, f,
                                       lam, weighted, nullptr, half, a_out, a_stride, b_out, nu_out, overflow, st, b,
-                                      e, k > 1, k == P);
+                                      e, k > 1, k == P, sym);
         if (rc != CMF_OK) return rc;
     }
     return CMF_OK;

@@ -562,7 +562,10 @@ __device__ __forceinline__ uint32_t elect_one() {
 // MMA per 16-row K-step; releases stages with tcgen05.commit.  Buffer b
 // occupies columns [b*N, (b+1)*N).  The next row's extent is loaded one row
 // ahead so the indptr latency stays off the issue loop.
-template <int NST, bool SPLIT, int NBUF, bool WEIGHTED = false>
+// SYM (split operands only): two chains per row, H H^T into [2bN, 2bN + N) and
+// S = H^T L into [2bN + N, 2bN + 2N); the epilogue adds S^T (= the L H^T term),
+// so each K-step reads its operands from shared memory twice instead of three times.
+template <int NST, bool SPLIT, int NBUF, bool WEIGHTED = false, bool SYM = false>
 __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, SPLIT, NBUF> &pp, uint32_t tmem_base,
                                           int N, int64_t row0, int64_t rstride, uint32_t cons_full = 0,
                                           int ncons = 0) {
@@ -590,7 +593,7 @@ __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, S
             const int b = rowc % NBUF;
             mbar_wait(pp.tempty(b), ((rowc / NBUF) & 1) ^ 1);
             tc_fence_after();
-            const uint32_t tmem_d = tmem_base + b * N;
+            const uint32_t tmem_d = tmem_base + b * N * (SYM ? 2 : 1);
             uint32_t acc = 0;
             for (int64_t q0 = s0; q0 < s1; q0 += KS, ++it) {
                 const int s = it % NST;
@@ -607,7 +610,9 @@ __device__ __forceinline__ void issue_mma(const GatherArgs &g, const Pipe<NST, S
                             continue;
                         }
                         tc_mma(tmem_d, d, d, idesc, acc | kk);
-                        if (SPLIT) {  // + H L^T + L H^T
+                        if (SPLIT && SYM) {  // S = H^T L in the second accumulator
+                            tc_mma(tmem_d + N, d, d + kLoStep, idesc, acc | kk);
+                        } else if (SPLIT) {  // + H L^T + L H^T
                             tc_mma(tmem_d, d, d + kLoStep, idesc, 1);
                             tc_mma(tmem_d, d + kLoStep, d, idesc, 1);
                         }

@@ -230,14 +230,15 @@ def test_exact_route_long_rows_factor_bar(oracle, cuda_device):
         assert np.linalg.norm(t_g - t_o) / np.linalg.norm(t_o) < 1e-4, (epoch, "t")
 
 
-@pytest.mark.parametrize("passes", ["2", "3", "5"])
-def test_exact_route_multipass_gram(oracle, cuda_device, monkeypatch, passes):
+@pytest.mark.parametrize("passes,sym", [("2", "0"), ("3", "0"), ("5", "0"), ("1", "1"), ("3", "1")])
+def test_exact_route_multipass_gram(oracle, cuda_device, monkeypatch, passes, sym):
     """The split-precision Gram in P passes over fixed-side id ranges
     (cmf_gram_assemble_tc_ws: the exact route's item side, whose hi + lo shadow
-    exceeds L2) against one pass and against the CPU oracle: items rated only
+    exceeds L2), and with the SYM accumulators (H H^T and S = H^T L, the copy-out
+    adds S^T), against one plain pass and against the CPU oracle: items rated only
     inside one id range (empty segments in the other passes) and items without
-    ratings included; factors within 1e-4 of the oracle, one pass vs P passes
-    to fp32 summation order."""
+    ratings included; factors within 1e-4 of the oracle, the variants vs one
+    plain pass to fp32 summation order."""
     m, n, f = 1500, 300, 48
     t, _, _ = oracle.gen_synthetic(m, n, f, 0.5, 0.1, 4)
     keep = ~((t.item < 20) & (t.user >= m // 3)) & ~((t.item >= 20) & (t.item < 30)) & (t.item != 31)
@@ -250,8 +251,9 @@ def test_exact_route_multipass_gram(oracle, cuda_device, monkeypatch, passes):
     th_o = th0.copy()
     oracle.update_side(r.csc(), x, th_o, 0.05, "exact")
     outs = []
-    for p in ("1", passes):
+    for p, sy in (("1", "0"), (passes, sym)):
         monkeypatch.setenv("CMF_GRAM_PASSES", p)
+        monkeypatch.setenv("CMF_GRAM_SYM", sy)
         th = th0.copy()
         cmfb.update_side(sr.csc_view(), x, th, 0.05, solver)
         outs.append(th)
