@@ -42,7 +42,10 @@ namespace tc {
 // ---------------------------------------------------------------------------
 // Batched CG over packed binary16 systems (the two-step route's K3: replaces
 // solvers._cg_batch for precision="fp16", solvers.py:121-145, 205-247).
-// Three 128-thread groups per CTA, two CTAs per SM; each group double-buffers
+// One CTA per SM with as many 128-thread groups as TMEM (a KP/2-column binary16
+// slot + a 16-column result block each) and shared memory allow: 7 at f = 100
+// (6 systems in flight per SM with the earlier 2 x 3 shape: 3.17 -> 2.96 ms on
+// the Netflix user side, same box); each group double-buffers
 // its systems' packed lower triangles HBM -> shared memory with cp.async
 // (the only large read), expands row i of the symmetric matrix into its TMEM
 // slot in the tcgen05 A-operand layout (the stored binary16 values, no
@@ -61,11 +64,28 @@ struct CgTcArgs {
     int pipelined;  // CMF_CG_PIPELINED=1: one barrier per iteration (pipelined recurrence)
 };
 
-constexpr int CGT_GROUPS = 3;
-constexpr int CGT_THREADS = 128 * CGT_GROUPS;
+// CTA shape: CGT_GROUPS systems in flight per CTA, CGT_PER_SM CTAs per SM, each
+// CTA owning 512 / CGT_PER_SM TMEM columns (a 56-column binary16 slot and a
+// 16-column matvec result block per group at f = 100)
+#ifndef CMF_CGT_GROUPS
+#define CMF_CGT_GROUPS 7
+#endif
+constexpr int CGT_PER_SM = CMF_CGT_GROUPS <= 3 ? 2 : 1;
+constexpr int CGT_TMEM = 512 / CGT_PER_SM;
+template <int KP>  // per-group shared memory: matvec operand + double-buffered staging
+constexpr int cgt_group_bytes() {
+    return (MVB_BYTES + 2 * ((((KP * (KP - 1) / 2 + 128) * 2) + 127) & ~127) + 1023) & ~1023;
+}
+template <int KP>  // groups whose slots + result blocks fit the CTA's TMEM and whose scratch fits smem
+constexpr int cgt_groups() {
+    constexpr int by_tmem = 512 / (KP / 2 + 16), by_smem = (227 * 1024 - 2048) / cgt_group_bytes<KP>();
+    constexpr int g = CMF_CGT_GROUPS < by_tmem ? CMF_CGT_GROUPS : by_tmem;
+    return CGT_PER_SM == 2 ? CMF_CGT_GROUPS : (g < by_smem ? g : by_smem);
+}
 
 template <int KP>
-__global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_constant__ CgTcArgs g) {
+__global__ void __launch_bounds__(128 * cgt_groups<KP>(), CGT_PER_SM) cg_tc_kernel(const __grid_constant__ CgTcArgs g) {
+    constexpr int CGT_GROUPS = cgt_groups<KP>(), CGT_THREADS = 128 * CGT_GROUPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     const int f = g.f;
@@ -86,7 +106,7 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
         for (int q = 0; q < CGT_GROUPS; ++q) mbar_init(smem_u32(mvbars + q), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 256);
+    if (warp == 0) tmem_alloc(smem_u32(tmem_slot), CGT_TMEM);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -96,9 +116,9 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
     const int i = cg.i, gt = tid & 127;
     // TMEM: 16-column aligned slots (KP/2 packed columns each), then the 16-column
     // matvec results from a 32-column boundary
-    constexpr uint32_t SLOT = (KP / 2 + 15) / 16 * 16;
-    constexpr uint32_t DBASE = (CGT_GROUPS * SLOT + 31) / 32 * 32;
-    static_assert(DBASE + 16 * CGT_GROUPS <= 256, "cg_tc TMEM plan");
+    constexpr uint32_t SLOT = CGT_PER_SM == 1 ? KP / 2 : (KP / 2 + 15) / 16 * 16;
+    constexpr uint32_t DBASE = (CGT_GROUPS * SLOT + 15) / 16 * 16;
+    static_assert(DBASE + 16 * CGT_GROUPS <= CGT_TMEM, "cg_tc TMEM plan");
     const uint32_t a_tmem = tmem_base + grp * SLOT;
     const uint32_t dcol = tmem_base + DBASE + 16 * grp;
     const uint32_t slot_t = a_tmem + cg.lane_base;
@@ -200,7 +220,7 @@ __global__ void __launch_bounds__(CGT_THREADS, 2) cg_tc_kernel(const __grid_cons
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, 256);
+        tmem_dealloc(tmem_base, CGT_TMEM);
     }
 }
 
@@ -338,17 +358,18 @@ static int launch_cg_tc(const tc::CgTcArgs &g, cudaStream_t st) {
     (void)P;
     constexpr size_t SB = (((KP * (KP - 1) / 2 + 128) * 2) + 127) & ~127;  // as in cg_tc_kernel
     const size_t GS = (tc::MVB_BYTES + 2 * SB + 1023) & ~static_cast<size_t>(1023);
-    const size_t smem = 1024 + tc::CGT_GROUPS * GS + tc::CGT_GROUPS * 8 + 16;
+    constexpr int G = tc::cgt_groups<KP>();
+    const size_t smem = 1024 + G * GS + G * 8 + 16;
     auto k = tc::cg_tc_kernel<KP>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return set_error(CMF_ECUDA, "cg_tc smem attr: %s", cudaGetErrorString(e));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t grid = 2 * static_cast<int64_t>(sms);
-    const int64_t need = (g.nsys + tc::CGT_GROUPS - 1) / tc::CGT_GROUPS;
+    int64_t grid = tc::CGT_PER_SM * static_cast<int64_t>(sms);
+    const int64_t need = (g.nsys + G - 1) / G;
     if (grid > need) grid = need;
-    k<<<static_cast<unsigned>(grid), tc::CGT_THREADS, smem, st>>>(g);
+    k<<<static_cast<unsigned>(grid), 128 * G, smem, st>>>(g);
     return check_launch("cg_tc_kernel");
 }
 
