@@ -110,7 +110,7 @@ int cmf_gram_assemble_tc(const int64_t *indptr, const int32_t *indices, const fl
 /*
  * cmf_gram_assemble_tc with the rows' rating count and a device workspace:
  * the split-precision (fp32) Gram over long rows (nnz >= 1024 * nrows) whose
- * hi + lo shadow exceeds 56 MB runs P <= 8 passes over equal fixed-side id
+ * hi + lo shadow exceeds 72 MB runs P <= 8 passes over equal fixed-side id
  * ranges (each pass's shadow slice stays in L2), accumulating into a_out /
  * b_out; P - 1 arrays of nrows int64 segment bounds go to `ws`
  * (cmf_gram_tc_workspace_bytes; too small or NULL: one pass).  Same results as

@@ -516,8 +516,8 @@ int64_t gram_tc_passes(int64_t nrows, int64_t nnz, int64_t ncols, int W, bool sp
     if (const char *e = getenv("CMF_GRAM_PASSES"))  // A/B and tests (empty: automatic)
         if (*e) return atoi(e) > 1 ? (atoi(e) < 16 ? atoi(e) : 16) : 1;
     const int64_t shadow = ncols * W * 2 * (split ? 2 : 1);
-    if (!split || nnz < 1024 * nrows || shadow <= (int64_t(56) << 20)) return 1;
-    const int64_t p = (shadow + (int64_t(56) << 20) - 1) / (int64_t(56) << 20);
+    if (!split || nnz < 1024 * nrows || shadow <= (int64_t(72) << 20)) return 1;
+    const int64_t p = (shadow + (int64_t(72) << 20) - 1) / (int64_t(72) << 20);
     return p < 8 ? p : 8;
 }
 
