@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
     using PipeT = Pipe<STAGES, SPLIT, 2>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     constexpr int W = NCH * 8;
-    constexpr int WS = SYM ? W + 1 : W;  // staging row stride
+    // staging row stride: SYM odd (transposed reads); plain fp32 == 4 (mod 32) words,
+    // so that a warp's float4 row stores (rows i = lanes) are conflict-free
+    constexpr int WS = SYM ? W + 1 : (HALF_OUT ? W : W + ((4 - W) % 32 + 32) % 32);
     using SqT = typename std::conditional<HALF_OUT, __half, float>::type;
     const GatherArgs &ga = g.gather;
     const int f = ga.f;
@@ -249,7 +251,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gram_tc_kernel(const __grid_co
             if (g.b_out && i < f) g.b_out[u * f + i] = g.accumulate ? g.b_out[u * f + i] + bias : bias;
             // packed copy-out: entries k..k+3 per step (k % 4 == 0)
             const size_t row_off = static_cast<size_t>(u) * g.a_stride;
-            if (!g.base) {
+            if (!g.base && !HALF_OUT && !SYM) {
+                // plain fp32 (short rows on the exact route): one packed entry per lane
+                // per step -- consecutive lanes read consecutive staging words (no bank
+                // conflicts) and store 128 contiguous bytes per warp
+                float *dstf = reinterpret_cast<float *>(g.a_out) + row_off;
+                for (int64_t k = tid; k < P; k += EPI_THREADS) {
+                    const float e = static_cast<float>(sq[tab[k]]);
+                    dstf[k] = g.accumulate ? dstf[k] + e : e;
+                }
+            } else if (!g.base) {
                 for (int64_t k = 4 * tid; k < P; k += 4 * EPI_THREADS) {
                     const uint2 o = *reinterpret_cast<const uint2 *>(tab + k);
                     const int64_t nk = P - k;
@@ -481,7 +492,7 @@ int gram_tc_launch(const int64_t *indptr, const int32_t *indices, const float *v
     g.accumulate = accumulate;
     g.add_reg = add_reg;
     const int64_t P = packed_size(f);
-    const size_t ws_row = sym ? W + 1 : W;
+    const size_t ws_row = sym ? W + 1 : (half ? W : W + ((4 - W) % 32 + 32) % 32);  // as the kernel's WS
     const size_t sq_bytes = ((static_cast<size_t>(f) * ws_row * esz + (sym ? 4 : 0)) + 15) & ~static_cast<size_t>(15);
     const size_t tab_bytes = ((static_cast<size_t>(P) * 2) + 15) & ~static_cast<size_t>(15);
     const size_t sym_bytes = sym ? tab_bytes + ((static_cast<size_t>(f) * 8 + 15) & ~static_cast<size_t>(15)) : 0;
